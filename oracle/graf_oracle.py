@@ -1,0 +1,336 @@
+"""GRAF ambiguity-function ORACLE (float64, CPU) — TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s `cpu_baseline` /
+`--impl reference` leg may import or run anything under `oracle/`.  The product
+path (`paper_2506_22935_b200/`) never imports it and shares no code with it:
+the only module both sides use is `graf_inputs` (seeded waveform draws, no AF
+arithmetic).
+
+What it computes (citations: P:Lnnn = /root/reference/PAPER.md line nnn,
+S:Lnnn = SPEC.md line nnn; readings R# = DESIGN.md §2 / SURVEY.md §8(c)):
+
+  A[k,m] = sum_n s[n] * conj(s[n-k]) * exp(-2j*pi*m*n/M),
+           k in [-(N-1), N-1], m in [0, M)                     (north star;
+           aperiodic form of Eq. 2 P:L121 / Eq. 7, reading R1-R4)
+
+written out as the plain definition: the lag-product matrix R[k,n] =
+s[n]*conj(s[n-k]) (Eqs. 8-10, aperiodic: zero outside 0<=n-k<N)
+times the DFT matrix W[n,m] = exp(-2j*pi*((m*n) mod M)/M) (Eq. 11, P:L197-201,
+the "FFT over the time axis" written as its defining sum; a matrix product is
+the library primitive used for that sum).  There is NO FFT anywhere in this
+file.  Phases are reduced on exact integers ((m*n) mod M) before the
+exponential, so no phase error accumulates.
+
+Losses and gradient follow SURVEY.md §8(c) steps 4-8:
+  chi = |A|^2 (Eq. 12);  x = chi/E^2 if normalized (Eqs. 19-20 divide by
+  chi(0,0) = E^2, reading R6) else chi
+  S = sum_{Omega} w*chi;  LSE = c + T*log sum_{Omega} exp((x-c)/T), c = max x
+  L = lambda_isl*(S/E^2 | S) + lambda_psl*LSE              (Eq. 23 weighting)
+  f' = dL/dx = lambda_isl*w + lambda_psl*exp((x-LSE)/T) on Omega
+  G = dL/dA* = f'*A/E^2 (normalized) | f'*A (raw)          (Eq. 14)
+  H[k,n] = sum_m G[k,m]*exp(+2j*pi*m*n/M)                  ("IFFT (linear)", P:L230;
+                                                             S:L143 op_fft_rows adjoint)
+  g[p] = sum_k H[k,p]*s[p-k] + sum_k conj(H[k,p+k])*s[p+k]  (Eq. 15, "element-wise
+         - (2/E^3)*(sum_{Omega} f'*chi)*s   [normalized only]  multiplication gradient" P:L231)
+
+g is the Wirtinger cotangent dL/ds* (P:L219), so
+dL/dRe s = 2*Re g and dL/dIm s = 2*Im g.
+
+Parity pins: every function here is pinned by tests/test_oracle_pins.py against
+closed forms, invariants, brute force, numpy.fft, central finite differences
+and torch autograd (DESIGN.md §4 lists which pin covers which function).  No
+function is "parity unpinned".
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "LossSpec", "energy", "delay_rows", "centred_bins", "dft_matrix",
+    "lag_products", "ambiguity", "region", "loss_terms", "loss",
+    "loss_and_grad", "adjoint", "correlate", "surface", "loss_and_grad_chunked",
+    "periodic_ambiguity",
+]
+
+
+# ---------------------------------------------------------------------------
+# index conventions
+# ---------------------------------------------------------------------------
+def delay_rows(n: int, k_max: Optional[int] = None) -> np.ndarray:
+    """Delays k = -K..K with K = min(k_max, N-1) (north star: k in +-(N-1))."""
+    K = n - 1 if k_max is None else min(k_max, n - 1)
+    return np.arange(-K, K + 1)
+
+
+def centred(m: np.ndarray, M: int) -> np.ndarray:
+    """Centred Doppler index d in [-M/2, M/2): d = m for m < M/2 else m - M
+    (Alg. 1 step 5 fftshift; reading R5)."""
+    m = np.asarray(m)
+    return np.where(m < M // 2, m, m - M)
+
+
+def centred_bins(M: int, d_max: Optional[int] = None) -> np.ndarray:
+    """Raw Doppler bins m whose centred index satisfies |d| <= d_max."""
+    m = np.arange(M)
+    if d_max is None:
+        return m
+    return m[np.abs(centred(m, M)) <= d_max]
+
+
+def energy(s: np.ndarray) -> float:
+    """E = sum_n |s[n]|^2 (= chi(0,0)^(1/2))."""
+    s = np.asarray(s, dtype=np.complex128)
+    return float(np.sum(s.real ** 2 + s.imag ** 2))
+
+
+# ---------------------------------------------------------------------------
+# Step 3: the surface, as the plain definition (matrix form of the DFT sum)
+# ---------------------------------------------------------------------------
+def dft_matrix(n: int, M: int, bins: np.ndarray, sign: int = -1) -> np.ndarray:
+    """W[n, j] = exp(sign*2j*pi*((bins[j]*n) mod M)/M), n = 0..N-1."""
+    nn = np.arange(n, dtype=np.int64)[:, None]
+    mm = np.asarray(bins, dtype=np.int64)[None, :]
+    ph = (nn * mm) % M
+    return np.exp(sign * 2j * np.pi * ph / M)
+
+
+def lag_products(s: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """R[i, n] = s[n]*conj(s[n-k_i]) when 0 <= n-k_i < N, else 0 (Eqs. 8-10,
+    aperiodic reading R1).  rows: integer delays k."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    R = np.zeros((len(rows), n), dtype=np.complex128)
+    for i, k in enumerate(rows):
+        k = int(k)
+        lo, hi = max(0, k), min(n, n + k)
+        if lo < hi:
+            R[i, lo:hi] = s[lo:hi] * np.conj(s[lo - k:hi - k])
+    return R
+
+
+def ambiguity(s: np.ndarray, M: int, rows: Optional[np.ndarray] = None,
+              bins: Optional[np.ndarray] = None) -> np.ndarray:
+    """A[rows, bins] (complex128), direct O(N*|rows|*|bins|) evaluation."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    rows = delay_rows(n) if rows is None else np.asarray(rows)
+    bins = np.arange(M) if bins is None else np.asarray(bins)
+    return lag_products(s, rows) @ dft_matrix(n, M, bins)
+
+
+def surface(s: np.ndarray, M: int, kind: str = "c64", layout: str = "centered",
+            normalize_output: bool = False, k_begin: Optional[int] = None,
+            k_end: Optional[int] = None) -> np.ndarray:
+    """The forward-surface output the ABI writes: rows k_begin..k_end-1 (row
+    index k - k_begin), Doppler raw m or centred j = d + M/2 (Alg. 1 step 5,
+    P:L252).  kind: 'c64' -> A, 'abs' -> |A|, 'pow' -> |A|^2 (Alg. 1 step 4,
+    P:L251).  normalize_output divides A by E (Eq. 17 analogue: max chi = E^2,
+    P:L265-268, reading R6)."""
+    n = len(s)
+    kb = -(n - 1) if k_begin is None else k_begin
+    ke = n if k_end is None else k_end
+    A = ambiguity(s, M, rows=np.arange(kb, ke))
+    if normalize_output:
+        A = A / energy(s)
+    if layout == "centered":
+        A = np.roll(A, M // 2, axis=1)   # column j holds bin m = (j - M/2) mod M
+    if kind == "c64":
+        return A
+    if kind == "abs":
+        return np.abs(A)
+    if kind == "pow":
+        return np.abs(A) ** 2
+    raise ValueError(kind)
+
+
+# ---------------------------------------------------------------------------
+# Loss region and losses (steps 4-5)
+# ---------------------------------------------------------------------------
+@dataclass
+class LossSpec:
+    """Sidelobe region Omega_s (never defined by the paper; reading R7):
+    |k| <= k_max and |d| <= d_max, minus the mainlobe |k| <= ml_k and
+    |d| <= ml_d.  Optional separable weights w_k[k+N-1], w_d[d+M/2] (R8)."""
+    k_max: int
+    d_max: int
+    ml_k: int = 0
+    ml_d: int = 0
+    lambda_isl: float = 1.0
+    lambda_psl: float = 0.0
+    temperature: float = 0.01
+    normalize: int = 1
+    w_k: Optional[np.ndarray] = field(default=None, repr=False)
+    w_d: Optional[np.ndarray] = field(default=None, repr=False)
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "LossSpec":
+        return cls(**{k: v for k, v in d.items() if k in cls.__dataclass_fields__})
+
+
+def region(n: int, M: int, spec: LossSpec):
+    """rows (k), bins (m), mask [rows, bins] (bool), weights [rows, bins]."""
+    rows = delay_rows(n, spec.k_max)
+    bins = centred_bins(M, spec.d_max)
+    d = centred(bins, M)
+    mainlobe = (np.abs(rows)[:, None] <= spec.ml_k) & (np.abs(d)[None, :] <= spec.ml_d)
+    mask = ~mainlobe
+    wk = np.ones(len(rows)) if spec.w_k is None else np.asarray(spec.w_k, np.float64)[rows + n - 1]
+    wd = np.ones(len(bins)) if spec.w_d is None else np.asarray(spec.w_d, np.float64)[d + M // 2]
+    w = wk[:, None] * wd[None, :]
+    return rows, bins, mask, w
+
+
+def loss_terms(s: np.ndarray, M: int, spec: LossSpec) -> dict:
+    """All step 3-5 quantities for one waveform (dict of numpy values)."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    rows, bins, mask, w = region(n, M, spec)
+    if not mask.any():
+        raise ValueError("empty sidelobe region (S:L302)")
+    E = energy(s)
+    A = ambiguity(s, M, rows, bins)
+    chi = A.real ** 2 + A.imag ** 2
+    x = chi / E ** 2 if spec.normalize else chi
+    S = float(np.sum(w[mask] * chi[mask]))
+    T = spec.temperature
+    xm = x[mask]
+    c = float(np.max(xm))
+    Z = float(np.sum(np.exp((xm - c) / T)))
+    lse = c + T * np.log(Z)
+    isl = S / E ** 2 if spec.normalize else S
+    L = spec.lambda_isl * isl + spec.lambda_psl * lse
+    return dict(E=E, A=A, chi=chi, x=x, rows=rows, bins=bins, mask=mask, w=w,
+                S=S, isl=isl, c=c, Z=Z, lse=lse, loss=L, count=int(mask.sum()))
+
+
+def loss(s: np.ndarray, M: int, spec: LossSpec) -> float:
+    return loss_terms(s, M, spec)["loss"]
+
+
+# ---------------------------------------------------------------------------
+# Steps 6-8: the Wirtinger adjoint
+# ---------------------------------------------------------------------------
+def correlate(s: np.ndarray, H: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """Step 8 without the normalization term:
+    g[p] = sum_k H[k,p]*s[p-k] + sum_k conj(H[k,p+k])*s[p+k], valid indices only
+    (adjoint of R[k,n] = s[n]*conj(s[n-k]) w.r.t. s*, Eq. 15)."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    g = np.zeros(n, dtype=np.complex128)
+    for i, k in enumerate(rows):
+        k = int(k)
+        lo, hi = max(0, k), min(n, n + k)      # valid n (= p for term 1)
+        if lo >= hi:
+            continue
+        # term 1: p = n, uses s[p-k]
+        g[lo:hi] += H[i, lo:hi] * s[lo - k:hi - k]
+        # term 2: p = n - k, uses conj(H[k, p+k]) * s[p+k]
+        g[lo - k:hi - k] += np.conj(H[i, lo:hi]) * s[lo:hi]
+    return g
+
+
+def adjoint(s: np.ndarray, M: int, G: np.ndarray, rows: np.ndarray,
+            bins: Optional[np.ndarray] = None) -> np.ndarray:
+    """Generic backward (graf_af_backward): given G = dL/dA* on rows x bins,
+    return dL/ds* = steps 7-8 (no normalization term: A itself does not
+    depend on E)."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    bins = np.arange(M) if bins is None else np.asarray(bins)
+    H = np.asarray(G, dtype=np.complex128) @ dft_matrix(n, M, bins, sign=+1).T
+    return correlate(s, H, rows)
+
+
+def loss_and_grad(s: np.ndarray, M: int, spec: LossSpec):
+    """(L, g = dL/ds*, terms) for one waveform."""
+    t = loss_terms(s, M, spec)
+    s = np.asarray(s, dtype=np.complex128)
+    E, A, chi, x, mask, w = t["E"], t["A"], t["chi"], t["x"], t["mask"], t["w"]
+    T = spec.temperature
+    fp = np.zeros_like(chi)
+    fp[mask] = spec.lambda_isl * w[mask] + spec.lambda_psl * np.exp((x[mask] - t["lse"]) / T)
+    G = fp * A / E ** 2 if spec.normalize else fp * A
+    g = adjoint(s, M, G, t["rows"], t["bins"])
+    if spec.normalize:
+        g = g - (2.0 / E ** 3) * float(np.sum(fp[mask] * chi[mask])) * s
+    t["fprime"] = fp
+    t["sigma_g"] = (2.0 / E ** 3) * float(np.sum(np.abs(fp[mask]) * chi[mask])) * float(np.max(np.abs(s))) \
+        if spec.normalize else 0.0
+    return t["loss"], g, t
+
+
+def loss_and_grad_chunked(s: np.ndarray, M: int, spec: LossSpec, chunk_rows: int = 512,
+                          chunk_bins: int = 2048, threads_note: str = ""):
+    """Same quantities as loss_and_grad, for waveforms whose full surface does
+    not fit in memory (c5: 32767 x 16384 cells).  The row/bin chunking only
+    regroups independent dot products and exact partial sums (S, max, Z are
+    combined exactly); every A[k,m] is still the direct sum.  Two sweeps:
+    (1) S, c, Z over Omega; (2) recompute A, f', H and the correlation."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    rows_all, bins, mask_all, w_all = region(n, M, spec)
+    E = energy(s)
+    T = spec.temperature
+    S, c, Z, cnt = 0.0, -np.inf, 0.0, 0
+    # sweep 1
+    for r0 in range(0, len(rows_all), chunk_rows):
+        rows = rows_all[r0:r0 + chunk_rows]
+        Rm = lag_products(s, rows)
+        for b0 in range(0, len(bins), chunk_bins):
+            bb = bins[b0:b0 + chunk_bins]
+            A = Rm @ dft_matrix(n, M, bb)
+            chi = A.real ** 2 + A.imag ** 2
+            x = chi / E ** 2 if spec.normalize else chi
+            msk = mask_all[r0:r0 + chunk_rows, b0:b0 + chunk_bins]
+            w = w_all[r0:r0 + chunk_rows, b0:b0 + chunk_bins]
+            S += float(np.sum(w[msk] * chi[msk]))
+            cnt += int(msk.sum())
+            if msk.any():
+                cm = float(np.max(x[msk]))
+                if cm > c:
+                    Z = Z * np.exp((c - cm) / T)
+                    c = cm
+                Z += float(np.sum(np.exp((x[msk] - c) / T)))
+    lse = c + T * np.log(Z)
+    isl = S / E ** 2 if spec.normalize else S
+    L = spec.lambda_isl * isl + spec.lambda_psl * lse
+    # sweep 2
+    g = np.zeros(n, dtype=np.complex128)
+    fchi = 0.0
+    afchi = 0.0
+    for r0 in range(0, len(rows_all), chunk_rows):
+        rows = rows_all[r0:r0 + chunk_rows]
+        Rm = lag_products(s, rows)
+        H = np.zeros((len(rows), n), dtype=np.complex128)
+        for b0 in range(0, len(bins), chunk_bins):
+            bb = bins[b0:b0 + chunk_bins]
+            A = Rm @ dft_matrix(n, M, bb)
+            chi = A.real ** 2 + A.imag ** 2
+            x = chi / E ** 2 if spec.normalize else chi
+            msk = mask_all[r0:r0 + chunk_rows, b0:b0 + chunk_bins]
+            w = w_all[r0:r0 + chunk_rows, b0:b0 + chunk_bins]
+            fp = np.where(msk, spec.lambda_isl * w + spec.lambda_psl * np.exp((x - lse) / T), 0.0)
+            fchi += float(np.sum(fp * chi))
+            afchi += float(np.sum(np.abs(fp) * chi))
+            G = fp * A / E ** 2 if spec.normalize else fp * A
+            H += G @ dft_matrix(n, M, bb, sign=+1).T
+        g += correlate(s, H, rows)
+    if spec.normalize:
+        g = g - (2.0 / E ** 3) * fchi * s
+    sigma_g = (2.0 / E ** 3) * afchi * float(np.max(np.abs(s))) if spec.normalize else 0.0
+    return L, g, dict(E=E, S=S, isl=isl, c=c, Z=Z, lse=lse, loss=L, count=cnt, sigma_g=sigma_g)
+
+
+# ---------------------------------------------------------------------------
+# The paper's own periodic surface (Eq. 2), used by the fold-identity pin
+# ---------------------------------------------------------------------------
+def periodic_ambiguity(s: np.ndarray) -> np.ndarray:
+    """X[k,m] = sum_n s[n]*conj(s[(n-k) mod N])*exp(+2j*pi*m*n/N), k,m in [0,N)
+    — Eq. 2 inside the |.|^2 exactly as printed (periodic, e^{+j}, M = N)."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    R = np.stack([s * np.conj(np.roll(s, k)) for k in range(n)])
+    return R @ dft_matrix(n, n, np.arange(n), sign=+1)
