@@ -1,0 +1,156 @@
+/*
+ * graf.h — C ABI of the B200 (sm_100a) GRAF ambiguity-function hot path.
+ *
+ * Operation (BASELINE.json north_star; aperiodic, M-bin, e^{-j} form of the
+ * paper's Eq. 2, PAPER.md L121 / Eq. 7, readings R1-R5 in DESIGN.md §2):
+ *
+ *   A[k,m] = sum_{n} s[n] * conj(s[n-k]) * exp(-2*pi*j*m*n/M),
+ *            k in [-(N-1), N-1], m in [0, M), terms with n-k outside [0,N) are 0.
+ *
+ * computed as delay-lag products (Eqs. 8-10) followed by a
+ * length-M Doppler FFT per delay row (Eq. 11; Algorithm 1 steps 1-3,
+ * L245-250), its magnitude (Eq. 12; Alg. 1 step 4), the sidelobe losses
+ * ISL (Eq. 20) and log-sum-exp soft-PSL (smoothed Eq. 19)
+ * over a region mask, and the Wirtinger adjoint dL/ds* (Eqs. 13-15).
+ *
+ * Conventions shared by every entry point:
+ *  - All data pointers (s, surface, dA, grad, loss, partials unless stated,
+ *    w_k, w_d, workspace) are DEVICE pointers owned by the caller.  The
+ *    library never allocates or frees device memory, never synchronises the
+ *    device, and enqueues all work on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  Results are complete when the stream
+ *    reaches them.
+ *  - Complex data are complex64 interleaved (re, im float32), row-major:
+ *    s [B][N]; surface / dA [B][k_end-k_begin][M] with row index k-k_begin and
+ *    Doppler column m (GRAF_DOPPLER_RAW) or j = d + M/2 with centred Doppler
+ *    d = m (m < M/2) else m - M (GRAF_DOPPLER_CENTERED, Alg. 1 step 5 fftshift,
+ *    L252).  Pointers must be 16-byte aligned.
+ *  - Gradients are Wirtinger cotangents g = dL/ds* (PAPER
+ *    L219): dL/dRe s = 2 Re g, dL/dIm s = 2 Im g.  Outputs are overwritten,
+ *    never accumulated.  Torch's complex .grad equals 2*g.
+ *  - Reentrant: no mutable global state except an immutable per-device table
+ *    of M-th roots of unity, initialised once per device on first use.
+ *  - Deterministic: fixed reduction order, no floating-point atomics; a call
+ *    repeated on the same inputs returns bitwise-identical outputs.
+ *  - Errors: argument checks happen on the host before any launch and return a
+ *    non-OK status with a message in graf_last_error() (thread-local).  A CUDA
+ *    launch failure returns GRAF_ECUDA.  Value-dependent problems (E = 0,
+ *    NaN/Inf in s) are not detected: they propagate as IEEE NaN.
+ *  - v1 device limits: M a power of two with max(N,2) <= M <= 16384; N >= 1.
+ */
+#ifndef GRAF_H_
+#define GRAF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRAF_ABI_VERSION 1
+#define GRAF_MAX_M 16384
+
+typedef enum {
+  GRAF_OK = 0,
+  GRAF_EINVAL = 1,        /* malformed argument (sizes, ranges, NULL, alignment) */
+  GRAF_EUNSUPPORTED = 2,  /* well-formed but outside v1 device limits (M > 16384, M < N, ...) */
+  GRAF_ECUDA = 3,         /* a CUDA runtime call or launch failed */
+  GRAF_ENONFINITE = 4,    /* reserved (debug scans) */
+  GRAF_EWORKSPACE = 5     /* ws_bytes < graf_workspace_bytes(...) */
+} graf_status;
+
+typedef enum {
+  GRAF_OUT_NONE = 0,
+  GRAF_OUT_C64 = 1,       /* A (complex64) */
+  GRAF_OUT_ABS_F32 = 2,   /* |A| (float32) */
+  GRAF_OUT_POW_F32 = 3    /* chi = |A|^2 (float32), Alg. 1 step 4 */
+} graf_out_kind;
+
+typedef enum { GRAF_DOPPLER_RAW = 0, GRAF_DOPPLER_CENTERED = 1 } graf_doppler_layout;
+
+/* Problem geometry and surface output. */
+typedef struct {
+  int32_t abi_version;      /* must equal GRAF_ABI_VERSION */
+  int32_t n;                /* N >= 1: waveform length */
+  int32_t m;                /* M: Doppler bins, power of two, max(N,2) <= M <= 16384 */
+  int32_t out_kind;         /* graf_out_kind of `surface` (GRAF_OUT_NONE: no surface) */
+  int64_t batch;            /* B >= 1 waveforms */
+  int32_t k_begin, k_end;   /* surface / dA delay-row window, -(N-1) <= k_begin < k_end <= N */
+  int32_t doppler_layout;   /* graf_doppler_layout of surface and dA */
+  int32_t normalize_output; /* 1: surface holds A/E, |A|/E, chi/E^2 (Eq. 17 analogue: max chi = E^2, L265-268) */
+  int32_t shard_index;      /* delay sharding of the LOSS rows: this call handles the folded */
+  int32_t shard_count;      /*   delay rows k >= 0 with k % shard_count == shard_index (0/1 = all) */
+} graf_af_desc;
+
+/* Loss over the sidelobe region Omega_s (never defined by the paper,
+ * reading R7):  |k| <= k_max, |d| <= d_max, minus the mainlobe |k| <= ml_k && |d| <= ml_d.
+ *   x   = chi/E^2 (normalize = 1, Eqs. 19-20 divide by chi(0,0) = E^2) or chi (0)
+ *   ISL = sum_{Omega} w*x,  w = w_k[k+N-1] * w_d[d+M/2] (NULL = 1)        (Eq. 20)
+ *   softPSL = T*log sum_{Omega} exp(x/T)                                   (Eq. 19, smoothed)
+ *   L   = lambda_isl*ISL + lambda_psl*softPSL per waveform                 (Eq. 23 weights, L313)
+ * The row-folding (k >= 0 only) used by the kernels requires symmetric weights:
+ * w_k[N-1+k] == w_k[N-1-k] and w_d[M/2+d] == w_d[M/2-d]; the caller guarantees it. */
+typedef struct {
+  int32_t k_max, d_max;     /* >= 0 */
+  int32_t ml_k, ml_d;       /* mainlobe half-widths, >= 0 */
+  const float* w_k;         /* optional device [2N-1] delay weights */
+  const float* w_d;         /* optional device [M] Doppler weights */
+  float lambda_isl, lambda_psl;
+  float temperature;        /* T > 0 (read iff lambda_psl != 0) */
+  int32_t normalize;        /* 1 (default reading R6) or 0 (raw chi) */
+} graf_loss_desc;
+
+/* Per-waveform partial sums over the rows a call covered (exactly combinable
+ * across delay shards with graf_combine_partials):
+ *   isl_sum = sum w*chi (raw numerator);  lse_max = max x;
+ *   lse_sum = sum exp((x - lse_max)/T);   cen_sum = sum expm1((x - xbar)/T) with
+ *   xbar = (M-1)/|Omega| when Omega is constant-sum (reading R13), else 0. */
+typedef struct { double isl_sum, lse_max, lse_sum, cen_sum; } graf_partials;
+
+int32_t graf_abi_version(void);
+const char* graf_status_string(graf_status status);
+const char* graf_last_error(void);
+
+/* Bytes of device workspace the call with these descriptors needs (0 on
+ * invalid descriptors).  Same value for graf_af_forward, graf_af_loss_grad and
+ * graf_af_backward with the same descriptors; loss may be NULL. */
+size_t graf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss);
+
+/* Forward.  Writes the surface window (if af->out_kind != NONE; `surface` must
+ * then be non-NULL) and, if `loss` != NULL, this shard's graf_partials[B] into
+ * `partials` (device).  Kernels: lag product -> Stockham FFT -> epilogue. */
+graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss,
+                            const void* s, void* surface, graf_partials* partials,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* Loss and gradient.  `global` = combined partials [B] of ALL shards (device), or
+ * NULL to compute them here (unsharded call).  Writes loss[B] (double, may be
+ * NULL) and grad[B][N] = dL/ds* restricted to this shard's delay rows, including
+ * this shard's share of the normalization term, so the SUM over shards is the
+ * full gradient.  Optionally writes the surface window too (af->out_kind).
+ * ISL-only losses (lambda_psl == 0) run as ONE fused pass (forward, epilogue,
+ * inverse FFT, delay correlation); soft-PSL needs the global LSE and runs two. */
+graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss,
+                              const void* s, const graf_partials* global,
+                              double* loss_out, void* grad, void* surface,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* Generic adjoint for arbitrary losses of A:  given dA = dL/dA* over the rows
+ * [k_begin, k_end) (complex64 [B][rows][M], af->doppler_layout), write
+ * grad[B][N] = dL/ds* = sum_k (term1 + term2) of the inverse Doppler DFT of dA
+ * ("IFFT operation (linear)", Eq. 15).  Linear in dA. */
+graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA,
+                             void* grad, void* ws, size_t ws_bytes, void* stream);
+
+/* Combine per-shard partials shards[G][B] into out[B] in shard order
+ * (deterministic).  on_device = 1: both arrays are device pointers and the work
+ * is enqueued on `stream`; 0: both are host pointers, computed synchronously. */
+graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partials* shards,
+                                  int32_t G, int64_t B, graf_partials* out,
+                                  int32_t on_device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAF_H_ */

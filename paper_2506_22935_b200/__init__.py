@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) GRAF ambiguity-function hot path (arXiv 2506.22935).
+
+Public API (thin binding of include/graf.h; all compute in libgraf.so):
+    af_forward, af_loss_grad, af_backward, combine_partials, LossSpec,
+    af / af_loss (torch autograd), sharding.* (torch.distributed layers).
+"""
+from ._lib import GrafError, lib  # noqa: F401
+from .graf import (AF, AFLoss, LossSpec, af, af_backward, af_forward, af_loss,  # noqa: F401
+                   af_loss_grad, combine_partials, workspace_bytes)
+
+__all__ = ["AF", "AFLoss", "LossSpec", "af", "af_backward", "af_forward", "af_loss", "af_loss_grad",
+           "combine_partials", "workspace_bytes", "GrafError", "lib"]

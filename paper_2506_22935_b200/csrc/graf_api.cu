@@ -1,0 +1,573 @@
+// graf_api.cu — the C ABI (include/graf.h): argument checks, launch planning,
+// workspace layout and the kernel sequences of each entry point.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/graf.h"
+#include "graf_kernels.cuh"
+
+namespace graf {
+namespace {
+
+thread_local std::string t_last_error;
+
+graf_status fail(graf_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+graf_status fail(graf_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  return st;
+}
+
+graf_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(GRAF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// one-time per-device twiddle table (immutable afterwards)
+// ---------------------------------------------------------------------------
+constexpr int kMaxDev = 64;
+std::once_flag g_tw_once[kMaxDev];
+cudaError_t g_tw_err[kMaxDev];
+
+cudaError_t ensure_twiddles() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  std::call_once(g_tw_once[dev], [dev] {
+    std::vector<float2> h(kMaxM);
+    for (int i = 0; i < kMaxM; ++i) {
+      // exp(-2 pi i * i / kMaxM) from exact integer phases, rounded once to float
+      const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)i / kMaxM;
+      h[i] = make_float2((float)cosl(a), (float)sinl(a));
+    }
+    g_tw_err[dev] = cudaMemcpyToSymbol(g_tw, h.data(), sizeof(float2) * kMaxM);
+  });
+  return g_tw_err[dev];
+}
+
+// ---------------------------------------------------------------------------
+// launch plan
+// ---------------------------------------------------------------------------
+struct Plan {
+  int M = 0, threads = 0, S = 0, T = 0, P = 1;
+  int U = 0, row_lo = 0, row_step = 1;
+  bool s_smem = true, g_smem = true;
+  size_t smem = 0;
+  size_t off_part = 0, off_gpart = 0, off_comb = 0, total = 0;
+};
+
+struct CfgInfo {
+  int M, E, T, S, threads, XS;
+  bool s_smem, g_smem;
+};
+
+template <int M>
+CfgInfo cfg_info() {
+  using C = Cfg<M>;
+  return CfgInfo{M, C::E, C::T, C::S, C::THREADS, C::XS, C::S_SMEM, C::G_SMEM};
+}
+
+bool cfg_for(int M, CfgInfo* ci) {
+  switch (M) {
+    case 2: *ci = cfg_info<2>(); return true;
+    case 4: *ci = cfg_info<4>(); return true;
+    case 8: *ci = cfg_info<8>(); return true;
+    case 16: *ci = cfg_info<16>(); return true;
+    case 32: *ci = cfg_info<32>(); return true;
+    case 64: *ci = cfg_info<64>(); return true;
+    case 128: *ci = cfg_info<128>(); return true;
+    case 256: *ci = cfg_info<256>(); return true;
+    case 512: *ci = cfg_info<512>(); return true;
+    case 1024: *ci = cfg_info<1024>(); return true;
+    case 2048: *ci = cfg_info<2048>(); return true;
+    case 4096: *ci = cfg_info<4096>(); return true;
+    case 8192: *ci = cfg_info<8192>(); return true;
+    case 16384: *ci = cfg_info<16384>(); return true;
+    default: return false;
+  }
+}
+
+constexpr int kNumSM = 148;  // B200; the plan is a pure function of the descriptors
+
+bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+graf_status check_af(const graf_af_desc* af) {
+  if (!af) return fail(GRAF_EINVAL, "af descriptor is NULL");
+  if (af->abi_version != GRAF_ABI_VERSION)
+    return fail(GRAF_EINVAL, "abi_version %d != %d", af->abi_version, GRAF_ABI_VERSION);
+  if (af->n < 1) return fail(GRAF_EINVAL, "N = %d < 1", af->n);
+  if (af->batch < 1) return fail(GRAF_EINVAL, "batch = %lld < 1", (long long)af->batch);
+  if (!is_pow2(af->m) || af->m < 2) return fail(GRAF_EINVAL, "M = %d is not a power of two >= 2", af->m);
+  if (af->m > GRAF_MAX_M) return fail(GRAF_EUNSUPPORTED, "M = %d > %d", af->m, GRAF_MAX_M);
+  if (af->m < af->n) return fail(GRAF_EUNSUPPORTED, "M = %d < N = %d (v1 device path needs M >= N)", af->m, af->n);
+  if (af->out_kind < GRAF_OUT_NONE || af->out_kind > GRAF_OUT_POW_F32)
+    return fail(GRAF_EINVAL, "out_kind %d", af->out_kind);
+  if (af->doppler_layout != GRAF_DOPPLER_RAW && af->doppler_layout != GRAF_DOPPLER_CENTERED)
+    return fail(GRAF_EINVAL, "doppler_layout %d", af->doppler_layout);
+  const int sc = af->shard_count <= 0 ? 1 : af->shard_count;
+  if (af->shard_index < 0 || af->shard_index >= sc)
+    return fail(GRAF_EINVAL, "shard_index %d not in [0, %d)", af->shard_index, sc);
+  return GRAF_OK;
+}
+
+graf_status check_window(const graf_af_desc* af) {
+  if (af->k_begin < -(af->n - 1) || af->k_end > af->n || af->k_begin >= af->k_end)
+    return fail(GRAF_EINVAL, "row window [%d, %d) not inside [-(N-1), N) = [%d, %d)", af->k_begin, af->k_end,
+                -(af->n - 1), af->n);
+  return GRAF_OK;
+}
+
+graf_status check_loss(const graf_af_desc* af, const graf_loss_desc* L) {
+  if (L->k_max < 0 || L->d_max < 0 || L->ml_k < 0 || L->ml_d < 0)
+    return fail(GRAF_EINVAL, "negative region bound");
+  if (L->normalize != 0 && L->normalize != 1) return fail(GRAF_EINVAL, "normalize must be 0 or 1");
+  if (L->lambda_psl != 0.f && !(L->temperature > 0.f)) return fail(GRAF_EINVAL, "temperature must be > 0");
+  if (!std::isfinite(L->lambda_isl) || !std::isfinite(L->lambda_psl))
+    return fail(GRAF_EINVAL, "non-finite lambda");
+  const int kl = std::min(L->k_max, af->n - 1);
+  const int dl = std::min(L->d_max, af->m / 2);
+  const bool nonempty = kl > L->ml_k || dl > L->ml_d;
+  if (!nonempty) return fail(GRAF_EINVAL, "empty sidelobe region (mainlobe covers the mask)");
+  return GRAF_OK;
+}
+
+bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+// fold the unfolded window [kb, ke) to |k|: a contiguous range [lo, hi]
+void folded_window(int kb, int ke, int* lo, int* hi) {
+  const int a = kb, z = ke - 1;
+  if (a <= 0 && z >= 0) {
+    *lo = 0;
+    *hi = std::max(-a, z);
+  } else if (a > 0) {
+    *lo = a;
+    *hi = z;
+  } else {
+    *lo = -z;
+    *hi = -a;
+  }
+}
+
+enum class Kind { Forward, LossGrad, Backward };
+
+Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
+  Plan pl;
+  CfgInfo ci;
+  cfg_for(af->m, &ci);
+  pl.M = af->m;
+  pl.threads = ci.threads;
+  pl.S = ci.S;
+  pl.T = ci.T;
+  pl.s_smem = ci.s_smem;
+  pl.g_smem = ci.g_smem;
+  const int N = af->n;
+  const int sc = af->shard_count <= 0 ? 1 : af->shard_count;
+  const bool grad = (kind != Kind::Forward);
+  if (kind == Kind::Backward) {
+    pl.row_lo = af->k_begin;
+    pl.row_step = 1;
+    pl.U = af->k_end - af->k_begin;
+  } else {
+    const bool surf = af->out_kind != GRAF_OUT_NONE;
+    const int kloss = L ? std::min(L->k_max, N - 1) : -1;
+    if (surf) {
+      int lo, hi;
+      folded_window(af->k_begin, af->k_end, &lo, &hi);
+      if (L) {
+        lo = 0;
+        hi = std::max(hi, kloss);
+      }
+      pl.row_lo = lo;
+      pl.row_step = 1;
+      pl.U = hi - lo + 1;
+    } else if (L) {
+      pl.row_lo = af->shard_index;
+      pl.row_step = sc;
+      pl.U = af->shard_index <= kloss ? (kloss - af->shard_index) / sc + 1 : 0;
+    } else {
+      pl.U = 0;
+    }
+  }
+  pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
+                              (grad && ci.g_smem ? (size_t)ci.S * N : 0));
+  int occ = std::min(2048 / ci.threads, 32);
+  occ = std::max(1, std::min<int>(occ, (int)((228 * 1024) / (pl.smem + 1024))));
+  const long long target = (long long)kNumSM * occ * 4;
+  const long long B = af->batch;
+  long long P = (target + B - 1) / B;
+  const long long maxP = std::max(1, (pl.U + ci.S - 1) / ci.S);
+  P = std::max(1LL, std::min(P, maxP));
+  pl.P = (int)P;
+  size_t off = 0;
+  pl.off_part = off;
+  off = align256(off + sizeof(double) * kPart * (size_t)B * pl.P);
+  pl.off_gpart = off;
+  if (grad) off = align256(off + sizeof(float2) * (size_t)B * pl.P * N);
+  pl.off_comb = off;
+  off = align256(off + sizeof(graf_partials) * (size_t)B);
+  pl.total = off;
+  return pl;
+}
+
+template <int M>
+cudaError_t launch_rows_t(const Plan& pl, RowParams rp, int B, cudaStream_t st) {
+  static std::once_flag once[kMaxDev];
+  static cudaError_t attr_err[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev], [dev] {
+    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+  });
+  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
+  for (int b0 = 0; b0 < B; b0 += 65535) {
+    rp.b0 = b0;
+    dim3 grid(pl.P, std::min(65535, B - b0));
+    af_rows_kernel<M><<<grid, pl.threads, pl.smem, st>>>(rp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_rows(const Plan& pl, const RowParams& rp, int B, cudaStream_t st) {
+  switch (pl.M) {
+    case 2: return launch_rows_t<2>(pl, rp, B, st);
+    case 4: return launch_rows_t<4>(pl, rp, B, st);
+    case 8: return launch_rows_t<8>(pl, rp, B, st);
+    case 16: return launch_rows_t<16>(pl, rp, B, st);
+    case 32: return launch_rows_t<32>(pl, rp, B, st);
+    case 64: return launch_rows_t<64>(pl, rp, B, st);
+    case 128: return launch_rows_t<128>(pl, rp, B, st);
+    case 256: return launch_rows_t<256>(pl, rp, B, st);
+    case 512: return launch_rows_t<512>(pl, rp, B, st);
+    case 1024: return launch_rows_t<1024>(pl, rp, B, st);
+    case 2048: return launch_rows_t<2048>(pl, rp, B, st);
+    case 4096: return launch_rows_t<4096>(pl, rp, B, st);
+    case 8192: return launch_rows_t<8192>(pl, rp, B, st);
+    case 16384: return launch_rows_t<16384>(pl, rp, B, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
+  const int N = af->n, M = af->m;
+  rp.loss_on = 1;
+  rp.kloss = std::min(L->k_max, N - 1);
+  rp.d_max = L->d_max;
+  rp.ml_k = L->ml_k;
+  rp.ml_d = L->ml_d;
+  rp.w_k = L->w_k;
+  rp.w_d = L->w_d;
+  rp.lam_isl = L->lambda_isl;
+  rp.lam_psl = L->lambda_psl;
+  rp.T = L->lambda_psl != 0.f ? L->temperature : 1.f;
+  rp.invT = 1.f / rp.T;
+  rp.normalize = L->normalize;
+  // reading R13: constant-sum region -> centred soft-PSL weights
+  const bool full = rp.kloss == N - 1 && L->d_max >= M / 2 && L->ml_k == 0 && L->ml_d == 0;
+  rp.centred = (L->normalize && !L->w_k && !L->w_d && full && L->lambda_psl != 0.f) ? 1 : 0;
+  rp.omega = (double)(2 * N - 1) * M - 1.0;
+  rp.xbar = (float)((M - 1) / rp.omega);
+}
+
+RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, void* ws) {
+  RowParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.s = static_cast<const float2*>(s);
+  rp.N = af->n;
+  rp.B = (int)af->batch;
+  rp.U = pl.U;
+  rp.row_lo = pl.row_lo;
+  rp.row_step = pl.row_step;
+  rp.kb = af->k_begin;
+  rp.ke = af->k_end;
+  rp.out_kind = af->out_kind;
+  rp.layout = af->doppler_layout;
+  rp.norm_out = af->normalize_output;
+  rp.shard_index = af->shard_index;
+  rp.shard_count = af->shard_count <= 0 ? 1 : af->shard_count;
+  rp.T = 1.f;
+  rp.invT = 1.f;
+  char* w = static_cast<char*>(ws);
+  rp.part = reinterpret_cast<double*>(w + pl.off_part);
+  rp.gpart = reinterpret_cast<float2*>(w + pl.off_gpart);
+  return rp;
+}
+
+graf_status common_checks(const graf_af_desc* af, const graf_loss_desc* L, const void* s, void* surface,
+                          bool need_surface_window) {
+  graf_status st = check_af(af);
+  if (st) return st;
+  if (af->batch > (1LL << 31) - 1) return fail(GRAF_EUNSUPPORTED, "batch too large");
+  if (!s) return fail(GRAF_EINVAL, "s is NULL");
+  if (!aligned8(s)) return fail(GRAF_EINVAL, "s is not 8-byte aligned");
+  if (af->out_kind != GRAF_OUT_NONE || need_surface_window) {
+    st = check_window(af);
+    if (st) return st;
+  }
+  if (af->out_kind != GRAF_OUT_NONE) {
+    if (!surface) return fail(GRAF_EINVAL, "out_kind set but surface is NULL");
+    if (!aligned8(surface)) return fail(GRAF_EINVAL, "surface is not 8-byte aligned");
+  }
+  if (L) {
+    st = check_loss(af, L);
+    if (st) return st;
+  }
+  return GRAF_OK;
+}
+
+graf_status check_ws(const Plan& pl, void* ws, size_t ws_bytes) {
+  if (ws_bytes < pl.total) return fail(GRAF_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, pl.total);
+  if (pl.total && !ws) return fail(GRAF_EINVAL, "workspace is NULL");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(GRAF_EINVAL, "workspace not 256-byte aligned");
+  return GRAF_OK;
+}
+
+graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, const void* s,
+                         void* ws, const graf_partials* global, double* loss, void* grad, bool norm_term,
+                         cudaStream_t st) {
+  FinalizeParams f;
+  std::memset(&f, 0, sizeof(f));
+  char* w = static_cast<char*>(ws);
+  f.s = static_cast<const float2*>(s);
+  f.part = reinterpret_cast<const double*>(w + pl.off_part);
+  f.gpart = reinterpret_cast<const float2*>(w + pl.off_gpart);
+  f.global = global;
+  f.P = pl.P;
+  f.N = af->n;
+  f.B = (int)af->batch;
+  f.normalize = L ? L->normalize : 0;
+  f.grad_norm_term = norm_term ? 1 : 0;
+  f.lam_isl = L ? L->lambda_isl : 0.f;
+  f.lam_psl = L ? L->lambda_psl : 0.f;
+  f.T = (L && L->lambda_psl != 0.f) ? L->temperature : 1.f;
+  f.invT = 1.f / f.T;
+  f.loss = loss;
+  f.grad = static_cast<float2*>(grad);
+  const long long B = af->batch;
+  for (long long b0 = 0; b0 < B; b0 += 65535) {
+    FinalizeParams fc = f;
+    const long long nb = std::min<long long>(65535, B - b0);
+    fc.s = f.s + b0 * af->n;
+    fc.part = f.part + b0 * pl.P * kPart;
+    fc.gpart = f.gpart + b0 * pl.P * (long long)af->n;
+    fc.global = global ? global + b0 : nullptr;
+    fc.loss = loss ? loss + b0 : nullptr;
+    fc.grad = grad ? f.grad + b0 * af->n : nullptr;
+    fc.B = (int)nb;
+    finalize_kernel<<<(unsigned)nb, 256, 0, st>>>(fc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "finalize_kernel launch");
+  }
+  return GRAF_OK;
+}
+
+graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, void* ws,
+                                graf_partials* out, cudaStream_t st) {
+  ReduceParams r;
+  r.part = reinterpret_cast<const double*>(static_cast<char*>(ws) + pl.off_part);
+  r.P = pl.P;
+  r.B = (int)af->batch;
+  r.T = L->lambda_psl != 0.f ? L->temperature : 1.f;
+  r.invT = 1.f / r.T;
+  r.out = out;
+  partials_reduce_kernel<<<(r.B + 127) / 128, 128, 0, st>>>(r);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "partials_reduce_kernel launch");
+}
+
+}  // namespace
+}  // namespace graf
+
+using namespace graf;
+
+extern "C" {
+
+int32_t graf_abi_version(void) { return GRAF_ABI_VERSION; }
+
+const char* graf_status_string(graf_status s) {
+  switch (s) {
+    case GRAF_OK: return "GRAF_OK";
+    case GRAF_EINVAL: return "GRAF_EINVAL: invalid argument";
+    case GRAF_EUNSUPPORTED: return "GRAF_EUNSUPPORTED: outside v1 device limits";
+    case GRAF_ECUDA: return "GRAF_ECUDA: CUDA error";
+    case GRAF_ENONFINITE: return "GRAF_ENONFINITE: non-finite value";
+    case GRAF_EWORKSPACE: return "GRAF_EWORKSPACE: workspace too small";
+    default: return "GRAF_UNKNOWN";
+  }
+}
+
+const char* graf_last_error(void) { return t_last_error.c_str(); }
+
+size_t graf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) {
+  if (check_af(af) != GRAF_OK) return 0;
+  if (loss && check_loss(af, loss) != GRAF_OK) return 0;
+  size_t need = make_plan(af, loss, Kind::LossGrad).total;
+  if (af->k_begin >= -(af->n - 1) && af->k_end <= af->n && af->k_begin < af->k_end)
+    need = std::max(need, make_plan(af, nullptr, Kind::Backward).total);
+  return need;
+}
+
+graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s, void* surface,
+                            graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
+  graf_status st = common_checks(af, loss, s, surface, false);
+  if (st) return st;
+  if (loss && !partials) return fail(GRAF_EINVAL, "loss given but partials is NULL");
+  const Plan pl = make_plan(af, loss, Kind::Forward);
+  if ((st = check_ws(pl, ws, ws_bytes))) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ensure_twiddles();
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  RowParams rp = base_params(af, s, pl, ws);
+  rp.mode = MODE_FWD;
+  rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
+  rp.grad = GRAD_NONE;
+  if (loss) fill_loss(rp, af, loss);
+  if (pl.U > 0) {
+    e = launch_rows(pl, rp, (int)af->batch, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (forward) launch");
+  }
+  if (loss) {
+    if (pl.U == 0) {
+      Plan p0 = pl;  // this shard owns no rows: identity partials (P = 0 records)
+      p0.P = 0;
+      return run_partials_reduce(af, loss, p0, ws, partials, cs);
+    }
+    return run_partials_reduce(af, loss, pl, ws, partials, cs);
+  }
+  return GRAF_OK;
+}
+
+graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+                              const graf_partials* global, double* loss_out, void* grad, void* surface, void* ws,
+                              size_t ws_bytes, void* stream) {
+  graf_status st = common_checks(af, loss, s, surface, false);
+  if (st) return st;
+  if (!loss) return fail(GRAF_EINVAL, "loss descriptor is NULL");
+  if (!grad) return fail(GRAF_EINVAL, "grad is NULL");
+  if (!aligned8(grad)) return fail(GRAF_EINVAL, "grad is not 8-byte aligned");
+  const Plan pl = make_plan(af, loss, Kind::LossGrad);
+  if ((st = check_ws(pl, ws, ws_bytes))) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ensure_twiddles();
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  if (pl.U == 0) {
+    e = cudaMemsetAsync(grad, 0, sizeof(float2) * (size_t)af->batch * af->n, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "zero grad");
+    if (loss_out && !global) return fail(GRAF_EINVAL, "shard with no rows cannot compute the loss without `global`");
+    // loss from global partials via the finalize path with P partial records absent
+  }
+  RowParams rp = base_params(af, s, pl, ws);
+  rp.mode = MODE_FWD;
+  fill_loss(rp, af, loss);
+  rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
+  graf_partials* comb = reinterpret_cast<graf_partials*>(static_cast<char*>(ws) + pl.off_comb);
+  const graf_partials* stats = global;
+  if (loss->lambda_psl == 0.f) {
+    rp.grad = GRAD_ISL;  // single fused pass (f' = lambda_isl * w known up front)
+    if (pl.U > 0) {
+      e = launch_rows(pl, rp, (int)af->batch, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (isl) launch");
+    }
+  } else {
+    if (!stats) {
+      RowParams r1 = rp;
+      r1.grad = GRAD_NONE;
+      r1.surface = nullptr;
+      e = launch_rows(pl, r1, (int)af->batch, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 1) launch");
+      if ((st = run_partials_reduce(af, loss, pl, ws, comb, cs))) return st;
+      stats = comb;
+    }
+    rp.grad = GRAD_PASS2;
+    rp.stats = stats;
+    if (pl.U > 0) {
+      e = launch_rows(pl, rp, (int)af->batch, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 2) launch");
+    }
+  }
+  if (pl.U == 0) {
+    if (loss_out) {
+      // no rows here: loss purely from the global partials
+      Plan p0 = pl;
+      p0.P = 0;
+      return run_finalize(af, loss, p0, s, ws, global, loss_out, nullptr, false, cs);
+    }
+    return GRAF_OK;
+  }
+  return run_finalize(af, loss, pl, s, ws, stats, loss_out, grad, true, cs);
+}
+
+graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
+                             size_t ws_bytes, void* stream) {
+  graf_status st = common_checks(af, nullptr, s, nullptr, true);
+  if (st) return st;
+  if (!dA || !aligned8(dA)) return fail(GRAF_EINVAL, "dA is NULL or not 8-byte aligned");
+  if (!grad || !aligned8(grad)) return fail(GRAF_EINVAL, "grad is NULL or not 8-byte aligned");
+  const Plan pl = make_plan(af, nullptr, Kind::Backward);
+  if ((st = check_ws(pl, ws, ws_bytes))) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ensure_twiddles();
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  RowParams rp = base_params(af, s, pl, ws);
+  rp.mode = MODE_ADJ;
+  rp.dA = static_cast<const float2*>(dA);
+  rp.grad = GRAD_ADJ;
+  e = launch_rows(pl, rp, (int)af->batch, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (adjoint) launch");
+  return run_finalize(af, nullptr, pl, s, ws, nullptr, nullptr, grad, false, cs);
+}
+
+graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partials* shards, int32_t G, int64_t B,
+                                  graf_partials* out, int32_t on_device, void* stream) {
+  if (!loss || !shards || !out) return fail(GRAF_EINVAL, "NULL argument");
+  if (G < 1 || B < 1) return fail(GRAF_EINVAL, "G = %d, B = %lld", G, (long long)B);
+  const float T = loss->lambda_psl != 0.f ? loss->temperature : 1.f;
+  if (!(T > 0.f)) return fail(GRAF_EINVAL, "temperature must be > 0");
+  const float invT = 1.f / T;
+  if (on_device) {
+    CombineParams c{shards, G, (int)B, invT, out};
+    combine_partials_kernel<<<(unsigned)((B + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(c);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "combine_partials_kernel launch");
+  }
+  for (int64_t b = 0; b < B; ++b) {
+    double S = 0, Z = 0, Cs = 0;
+    float m = -INFINITY;
+    for (int q = 0; q < G; ++q) {
+      const graf_partials& g = shards[(size_t)q * B + b];
+      S += g.isl_sum;
+      Cs += g.cen_sum;
+      const float m2 = (float)g.lse_max;
+      const double Z2 = g.lse_sum;
+      if (m2 == -INFINITY) continue;
+      if (m == -INFINITY) {
+        m = m2;
+        Z = Z2;
+      } else if (m2 > m) {
+        Z = Z * std::exp((double)(m - m2) * invT) + Z2;
+        m = m2;
+      } else {
+        Z = Z + Z2 * std::exp((double)(m2 - m) * invT);
+      }
+    }
+    out[b] = graf_partials{S, (double)m, Z, Cs};
+  }
+  return GRAF_OK;
+}
+
+}  // extern "C"

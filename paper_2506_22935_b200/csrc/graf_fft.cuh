@@ -1,0 +1,182 @@
+// graf_fft.cuh — register/shared-memory Stockham FFT building blocks for sm_100a.
+//
+// The Doppler DFT of each delay row (Eq. 11; Alg. 1 step 3,
+// L250) is an unnormalised length-M DFT, X[m] = sum_n x[n] e^{-2 pi i m n / M}.
+// The adjoint needs the unnormalised inverse, H[n] = sum_m G[m] e^{+2 pi i m n/M}
+// ("IFFT operation (linear)").
+//
+// Layout (one "row slot" = T = M/E threads): thread t holds E complex values in
+// registers, slot e <-> index t + e*T.  A Stockham autosort pass of radix R and
+// stride Ns takes, for butterfly j' = t + q*T (q < E/R), the R inputs
+// x[j' + r*M/R] = slot q + r*E/R, twiddles them by W_M^{(j' mod Ns) r M/(Ns R)},
+// runs an in-register radix-R DFT and writes y[(j'/Ns)*Ns*R + (j' mod Ns) + r*Ns].
+// Non-final passes exchange through shared memory (padded index y + (y >> log2 E),
+// conflict-free for every (M, E) used — simulated offline); the
+// final pass lands its outputs in the SAME slots (index t + e*T), so the
+// frequency-domain epilogue and the inverse FFT work in registers with no
+// reordering.  The same slot<->index map holds for time and frequency.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace graf {
+
+constexpr int kMaxM = 16384;
+
+// M-th roots of unity table, g_tw[i] = exp(-2 pi i * i / kMaxM), float32
+// correctly rounded from extended precision on the host (graf_api.cu).  The
+// library is one translation unit, so the definition lives here.
+__device__ float2 g_tw[kMaxM];
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// cos(2 pi j / 32), float32-rounded, first quadrant j = 0..8.
+__host__ __device__ constexpr float cos32_q(int j) {
+  return j == 0 ? 1.0f : j == 1 ? 9.807852507e-01f : j == 2 ? 9.238795042e-01f
+       : j == 3 ? 8.314695954e-01f : j == 4 ? 7.071067691e-01f : j == 5 ? 5.555702448e-01f
+       : j == 6 ? 3.826834261e-01f : j == 7 ? 1.950903237e-01f : 0.0f;
+}
+__host__ __device__ constexpr float cos32(int j) {
+  j = ((j % 32) + 32) % 32;
+  return j <= 8 ? cos32_q(j) : j <= 16 ? -cos32_q(16 - j) : j <= 24 ? -cos32_q(j - 16) : cos32_q(32 - j);
+}
+__host__ __device__ constexpr float sin32(int j) { return cos32(8 - j); }
+
+// z * W_R^K with W_R = exp(-2 pi i / R) (forward) or exp(+2 pi i / R) (inverse);
+// trivial twiddles (1, -i, -1, +i) cost no multiplies.  R <= 32.
+template <int K, int R, bool INV>
+__device__ __forceinline__ float2 twc(float2 z) {
+  constexpr int J = (((K * (32 / R)) % 32) + 32) % 32;
+  if constexpr (J == 0) {
+    return z;
+  } else if constexpr (J == 8) {
+    return INV ? make_float2(-z.y, z.x) : make_float2(z.y, -z.x);
+  } else if constexpr (J == 16) {
+    return make_float2(-z.x, -z.y);
+  } else if constexpr (J == 24) {
+    return INV ? make_float2(z.y, -z.x) : make_float2(-z.y, z.x);
+  } else {
+    constexpr float c = cos32(J);
+    constexpr float s = INV ? sin32(J) : -sin32(J);
+    return make_float2(z.x * c - z.y * s, z.x * s + z.y * c);
+  }
+}
+
+template <int K, int R, bool INV>
+__device__ __forceinline__ void dft_combine(float2* x, const float2* e, const float2* o) {
+  if constexpr (K < R / 2) {
+    const float2 t = twc<K, R, INV>(o[K]);
+    x[K] = cadd(e[K], t);
+    x[K + R / 2] = csub(e[K], t);
+    dft_combine<K + 1, R, INV>(x, e, o);
+  }
+}
+
+// In-register DFT of length R (natural order in and out): radix-4 leaves,
+// radix-2 decimation-in-time combination above them.
+template <int R, bool INV>
+__device__ __forceinline__ void dft(float2* x) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    const float2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const float2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
+    const float2 t2 = cadd(x[1], x[3]);
+    const float2 d = csub(x[1], x[3]);
+    const float2 t3 = INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);  // d * (-+i)
+    x[0] = cadd(t0, t2);
+    x[2] = csub(t0, t2);
+    x[1] = cadd(t1, t3);
+    x[3] = csub(t1, t3);
+  } else {
+    float2 e[R / 2], o[R / 2];
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) {
+      e[i] = x[2 * i];
+      o[i] = x[2 * i + 1];
+    }
+    dft<R / 2, INV>(e);
+    dft<R / 2, INV>(o);
+    dft_combine<0, R, INV>(x, e, o);
+  }
+}
+
+template <int E>
+struct Log2 {
+  static constexpr int value = E <= 1 ? 0 : 1 + Log2<E / 2>::value;
+};
+template <>
+struct Log2<1> {
+  static constexpr int value = 0;
+};
+
+template <int E>
+__device__ __forceinline__ int padded(int y) {
+  return y + (y >> Log2<E>::value);
+}
+
+// One Stockham pass (see header comment).  Non-final passes store to `sh`.
+template <int M, int E, int R, int NS, bool INV, bool LAST>
+__device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t) {
+  constexpr int T = M / E;
+  constexpr int Q = E / R;
+  constexpr int TWS = kMaxM / M;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    float2 x[R];
+    const int jp = t + q * T;
+    const int jm = jp & (NS - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = v[q + r * Q];
+    if constexpr (NS > 1) {
+      const int step = jm * (M / (NS * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        float2 w = g_tw[((step * r) & (M - 1)) * TWS];
+        if (INV) w.y = -w.y;
+        x[r] = cmul(x[r], w);
+      }
+    }
+    dft<R, INV>(x);
+    if constexpr (LAST) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q + r * Q] = x[r];
+    } else {
+      const int base = (jp / NS) * NS * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) sh[padded<E>(base + r * NS)] = x[r];
+    }
+  }
+}
+
+// Full length-M FFT on the register slots of one row slot.  SYNC() orders the
+// row slot's shared-memory exchange (warp sync, named barrier or CTA barrier).
+template <int M, int E, int NS, bool INV, class Sync>
+__device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, const Sync& sync) {
+  constexpr int T = M / E;
+  constexpr int REM = M / NS;
+  constexpr int R = REM >= E ? E : REM;
+  constexpr bool LAST = (NS * R == M);
+  stockham_pass<M, E, R, NS, INV, LAST>(v, sh, t);
+  if constexpr (!LAST) {
+    sync();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
+    sync();
+    fft_rows<M, E, NS * R, INV, Sync>(v, sh, t, sync);
+  }
+}
+
+}  // namespace graf

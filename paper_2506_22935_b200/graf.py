@@ -1,0 +1,239 @@
+"""Python binding of the GRAF C ABI (include/graf.h): argument marshalling only.
+
+Every step of the path runs in libgraf.so's CUDA kernels; torch supplies device
+memory, the current stream and (in `sharding.py`) process groups.  Function
+names follow the ABI: af_forward, af_loss_grad, af_backward, combine_partials.
+
+Gradient convention: the ABI returns g = dL/ds* (Wirtinger; SPEC.md L113-118,
+PAPER.md L219).  torch's complex autograd carries 2*dL/ds*, so the autograd
+Functions below multiply by 2 (SURVEY.md finding 7).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import torch
+
+from . import _lib as L
+
+__all__ = ["LossSpec", "af_forward", "af_loss_grad", "af_backward", "combine_partials",
+           "workspace_bytes", "AF", "AFLoss", "af", "af_loss"]
+
+_OUT = {None: L.OUT_NONE, "none": L.OUT_NONE, "c64": L.OUT_C64, "abs": L.OUT_ABS_F32, "pow": L.OUT_POW_F32}
+_LAYOUT = {"raw": L.DOPPLER_RAW, "centered": L.DOPPLER_CENTERED, "centred": L.DOPPLER_CENTERED}
+
+
+@dataclass
+class LossSpec:
+    """graf_loss_desc (include/graf.h): region |k|<=k_max, |d|<=d_max minus the
+    mainlobe |k|<=ml_k && |d|<=ml_d; L = lambda_isl*ISL + lambda_psl*softPSL."""
+    k_max: int
+    d_max: int
+    ml_k: int = 0
+    ml_d: int = 0
+    lambda_isl: float = 1.0
+    lambda_psl: float = 0.0
+    temperature: float = 0.01
+    normalize: int = 1
+    w_k: Optional[torch.Tensor] = None   # device float32 [2N-1], symmetric
+    w_d: Optional[torch.Tensor] = None   # device float32 [M], symmetric
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "LossSpec":
+        return cls(**{k: v for k, v in d.items() if k in cls.__dataclass_fields__})
+
+    def desc(self) -> L.LossDesc:
+        return L.LossDesc(int(self.k_max), int(self.d_max), int(self.ml_k), int(self.ml_d),
+                          _ptr(self.w_k), _ptr(self.w_d), float(self.lambda_isl),
+                          float(self.lambda_psl), float(self.temperature), int(self.normalize))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("graf: tensors must live on a CUDA device")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_s(s: torch.Tensor) -> torch.Tensor:
+    if s.dtype != torch.complex64:
+        raise TypeError("graf: s must be complex64")
+    if not s.is_cuda:
+        raise ValueError("graf: s must be a CUDA tensor (no CPU fallback)")
+    if s.dim() == 1:
+        s = s[None]
+    return s.contiguous()
+
+
+def _desc(s: torch.Tensor, M: int, out=None, layout="centered", k_begin=None, k_end=None,
+          normalize_output=False, shard=(0, 1)) -> L.AfDesc:
+    B, N = s.shape
+    kb = -(N - 1) if k_begin is None else int(k_begin)
+    ke = N if k_end is None else int(k_end)
+    return L.AfDesc(L.ABI_VERSION, int(N), int(M), _OUT[out], int(B), kb, ke, _LAYOUT[layout],
+                    int(bool(normalize_output)), int(shard[0]), int(shard[1]))
+
+
+def workspace_bytes(desc: L.AfDesc, loss: Optional[L.LossDesc]) -> int:
+    return int(L.lib().graf_workspace_bytes(ctypes.byref(desc), ctypes.byref(loss) if loss else None))
+
+
+class Workspace:
+    """Grow-only device workspace (the library never allocates)."""
+
+    def __init__(self):
+        self.buf: Optional[torch.Tensor] = None
+
+    def get(self, nbytes: int, device) -> Tuple[int, int]:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf.data_ptr(), self.buf.numel()
+
+
+_ws = Workspace()
+
+
+def _surface_alloc(desc: L.AfDesc, device) -> Optional[torch.Tensor]:
+    if desc.out_kind == L.OUT_NONE:
+        return None
+    rows = desc.k_end - desc.k_begin
+    dt = torch.complex64 if desc.out_kind == L.OUT_C64 else torch.float32
+    return torch.empty((desc.batch, rows, desc.m), dtype=dt, device=device)
+
+
+def af_forward(s: torch.Tensor, M: int, *, out: Optional[str] = "c64", layout: str = "centered",
+               k_begin: Optional[int] = None, k_end: Optional[int] = None, normalize_output: bool = False,
+               loss: Optional[LossSpec] = None, shard=(0, 1), ws: Optional[Workspace] = None,
+               surface: Optional[torch.Tensor] = None, stream=None):
+    """graf_af_forward: surface window and/or this shard's loss partials [B,4] (float64)."""
+    s = _check_s(s)
+    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard)
+    ld = loss.desc() if loss is not None else None
+    if surface is None:
+        surface = _surface_alloc(d, s.device)
+    partials = torch.empty((s.shape[0], 4), dtype=torch.float64, device=s.device) if loss is not None else None
+    nbytes = workspace_bytes(d, ld)
+    wp, wn = (ws or _ws).get(nbytes, s.device)
+    L.check(L.lib().graf_af_forward(ctypes.byref(d), ctypes.byref(ld) if ld else None,
+                                    ctypes.c_void_p(s.data_ptr()), _ptr(surface), _ptr(partials),
+                                    ctypes.c_void_p(wp), wn, _stream(stream)))
+    return surface, partials
+
+
+def af_loss_grad(s: torch.Tensor, M: int, loss: LossSpec, *, global_partials: Optional[torch.Tensor] = None,
+                 out: Optional[str] = None, layout: str = "centered", k_begin=None, k_end=None,
+                 normalize_output: bool = False, shard=(0, 1), ws: Optional[Workspace] = None,
+                 grad: Optional[torch.Tensor] = None, loss_out: Optional[torch.Tensor] = None,
+                 surface: Optional[torch.Tensor] = None, want_loss: bool = True, stream=None):
+    """graf_af_loss_grad -> (loss[B] float64, grad[B,N] complex64 = dL/ds*, surface or None)."""
+    s = _check_s(s)
+    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard)
+    ld = loss.desc()
+    B, N = s.shape
+    if grad is None:
+        grad = torch.empty((B, N), dtype=torch.complex64, device=s.device)
+    if loss_out is None and want_loss:
+        loss_out = torch.empty((B,), dtype=torch.float64, device=s.device)
+    if surface is None:
+        surface = _surface_alloc(d, s.device)
+    if global_partials is not None:
+        assert global_partials.dtype == torch.float64 and global_partials.shape == (B, 4)
+    nbytes = workspace_bytes(d, ld)
+    wp, wn = (ws or _ws).get(nbytes, s.device)
+    L.check(L.lib().graf_af_loss_grad(ctypes.byref(d), ctypes.byref(ld), ctypes.c_void_p(s.data_ptr()),
+                                      _ptr(global_partials), _ptr(loss_out), ctypes.c_void_p(grad.data_ptr()),
+                                      _ptr(surface), ctypes.c_void_p(wp), wn, _stream(stream)))
+    return loss_out, grad, surface
+
+
+def af_backward(s: torch.Tensor, M: int, dA: torch.Tensor, *, k_begin=None, k_end=None,
+                layout: str = "centered", ws: Optional[Workspace] = None, stream=None) -> torch.Tensor:
+    """graf_af_backward: dL/ds* from dA = dL/dA* over rows [k_begin, k_end)."""
+    s = _check_s(s)
+    if dA.dtype != torch.complex64 or not dA.is_cuda:
+        raise TypeError("graf: dA must be a complex64 CUDA tensor")
+    dA = dA.contiguous()
+    d = _desc(s, M, None, layout, k_begin, k_end)
+    B, N = s.shape
+    if dA.shape != (B, d.k_end - d.k_begin, M):
+        raise ValueError(f"dA shape {tuple(dA.shape)} != {(B, d.k_end - d.k_begin, M)}")
+    grad = torch.empty((B, N), dtype=torch.complex64, device=s.device)
+    nbytes = workspace_bytes(d, None)
+    wp, wn = (ws or _ws).get(nbytes, s.device)
+    L.check(L.lib().graf_af_backward(ctypes.byref(d), ctypes.c_void_p(s.data_ptr()),
+                                     ctypes.c_void_p(dA.data_ptr()), ctypes.c_void_p(grad.data_ptr()),
+                                     ctypes.c_void_p(wp), wn, _stream(stream)))
+    return grad
+
+
+def combine_partials(loss: LossSpec, shards: torch.Tensor, stream=None) -> torch.Tensor:
+    """graf_combine_partials: shards [G,B,4] float64 -> [B,4], in shard order."""
+    G, B, four = shards.shape
+    assert four == 4 and shards.dtype == torch.float64
+    shards = shards.contiguous()
+    out = torch.empty((B, 4), dtype=torch.float64, device=shards.device)
+    ld = loss.desc()
+    if shards.is_cuda:
+        L.check(L.lib().graf_combine_partials(ctypes.byref(ld), ctypes.c_void_p(shards.data_ptr()), G, B,
+                                              ctypes.c_void_p(out.data_ptr()), 1, _stream(stream)))
+    else:
+        L.check(L.lib().graf_combine_partials(ctypes.byref(ld), ctypes.c_void_p(shards.data_ptr()), G, B,
+                                              ctypes.c_void_p(out.data_ptr()), 0, None))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# torch autograd integration (§4.3 "Complex gradient handling", L274)
+# ---------------------------------------------------------------------------
+class AF(torch.autograd.Function):
+    """Differentiable complex surface A (rows [k_begin,k_end), layout)."""
+
+    @staticmethod
+    def forward(ctx, s, M, layout="centered", k_begin=None, k_end=None):
+        surf, _ = af_forward(s.detach(), M, out="c64", layout=layout, k_begin=k_begin, k_end=k_end)
+        ctx.save_for_backward(s)
+        ctx.cfg = (M, layout, k_begin, k_end, s.dim())
+        return surf if s.dim() == 2 else surf[0]
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (s,) = ctx.saved_tensors
+        M, layout, kb, ke, dim = ctx.cfg
+        g = grad_out if dim == 2 else grad_out[None]
+        # torch hands 2*dL/dA*; the adjoint is linear, so the result is torch's 2*dL/ds*.
+        gs = af_backward(s.detach(), M, g.to(torch.complex64), k_begin=kb, k_end=ke, layout=layout)
+        return (gs if dim == 2 else gs[0]), None, None, None, None
+
+
+class AFLoss(torch.autograd.Function):
+    """Per-waveform loss L_b (float64 [B]) with the fused kernels' gradient."""
+
+    @staticmethod
+    def forward(ctx, s, M, spec):
+        lo, g, _ = af_loss_grad(s.detach(), M, spec)
+        ctx.save_for_backward(g)
+        ctx.dim = s.dim()
+        return lo if s.dim() == 2 else lo[0]
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (g,) = ctx.saved_tensors
+        go = grad_out if ctx.dim == 2 else grad_out[None]
+        gs = 2.0 * go.to(torch.float32)[:, None] * g          # torch .grad = 2 dL/ds*
+        return (gs if ctx.dim == 2 else gs[0]), None, None
+
+
+def af(s, M, layout="centered", k_begin=None, k_end=None):
+    return AF.apply(s, M, layout, k_begin, k_end)
+
+
+def af_loss(s, M, spec: LossSpec):
+    return AFLoss.apply(s, M, spec)
