@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py — GRAF ambiguity-function hot path on B200 (BASELINE.json metric:
+"AF forward+loss+grad surfaces/sec (N x M cells/s) and % of HBM/FP32 roofline").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl graf|reference]
+
+A step = one forward + loss + gradient pass of the whole hot path (SURVEY.md
+§8(a) rows a0-a7, plus a8 when sharded) over one batch of seeded synthetic
+waveforms of the chosen BASELINE.json config (default: configs[1] = c2, B=256,
+N=M=256, masked ISL, fused single pass), called through the C ABI
+(graf_af_loss_grad).  Inputs are resident in HBM before timing; each timed step
+is a CUDA-graph replay of that call, timed with CUDA events on the launching
+stream, with L2 flushed (256 MiB memset) between steps outside the events.
+Multi-GPU (torchrun): batch sharding, every rank runs its own batch (weak
+scaling, no data-path collective); time = max over ranks.
+
+`--impl reference`: this build has no reference implementation (the paper
+ships no code); the reference arm is the float64 CPU oracle (oracle/), timed on
+the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from graf_inputs import CONFIGS, config_waveforms  # noqa: E402
+
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # B200_PROFILING.md: 148 SMs, 1965 MHz; 128 FP32 lanes/SM
+
+
+def workload(cid: int) -> dict:
+    cfg = CONFIGS[cid]
+    loss = dict(cfg["loss"])
+    note = ""
+    if cid in (1, 3):
+        # DESIGN.md R12: normalised full-plane ISL is identically M-1 with a zero
+        # gradient (volume identity); time the raw mode, whose gradient is real work.
+        loss["normalize"] = 0
+        note = "raw (unnormalised) full-plane ISL: the normalised one is constant (volume identity)"
+    N, M, B = cfg["N"], cfg["M"], cfg["B"]
+    rows = min(loss["k_max"], N - 1) + 1                       # folded delay rows k >= 0
+    ffts = 2 if loss["lambda_psl"] == 0 else 3                  # fused ISL: fwd+inv; soft-PSL: fwd | fwd+inv
+    flops = B * rows * ffts * 5.0 * M * math.log2(M)             # SURVEY.md §8(d) algorithmic FFT flops
+    surf_bytes = 0
+    if cfg["surface"]:
+        per = 8 if cfg["surface"] == "c64" else 4
+        surf_bytes = B * (2 * N - 1) * M * per
+    io_bytes = B * N * 8 * 2
+    return dict(cid=cid, cfg=cfg, loss=loss, N=N, M=M, B=B, rows=rows, ffts=ffts, flops=flops,
+                surf_bytes=surf_bytes, io_bytes=io_bytes, note=note,
+                launches=(2 if loss["lambda_psl"] == 0 else 4))
+
+
+def describe(w: dict) -> str:
+    c = w["cfg"]
+    L = w["loss"]
+    return (f"{c['name']}: B={w['B']} N={w['N']} M={w['M']} {c['family']}; "
+            f"{'surface ' + c['surface'] + ' + ' if c['surface'] else ''}"
+            f"ISL x{L['lambda_isl']} + softPSL x{L['lambda_psl']} (T={L['temperature']}) on |k|<={L['k_max']}, "
+            f"|d|<={L['d_max']} minus |k|<={L['ml_k']}&|d|<={L['ml_d']}, normalize={L['normalize']}")
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(gpu_index)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        self.t0 = time.time()
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def read_traffic(cid: int):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get(f"c{cid}")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(w: dict, budget_s: float = 12.0) -> dict:
+    """The float64 oracle as it stands, on the host cores, on a bounded sample."""
+    from oracle import graf_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    spec = O.LossSpec.from_dict(w["loss"])
+    N, M = w["N"], w["M"]
+    done, t0 = 0, time.perf_counter()
+    b = 0
+    while True:
+        s = config_waveforms(w["cid"], batch=1, start=b % w["B"])[0]
+        if w["N"] * w["M"] > 4096 * 8192:          # c5: the direct sum takes minutes per waveform
+            s_small = s
+            O.loss_and_grad_chunked(s_small, M, spec)
+        else:
+            O.loss_and_grad(s, M, spec)
+            if w["cfg"]["surface"]:
+                O.surface(s, M, w["cfg"]["surface"], "centered")
+        done += 1
+        b += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or done >= w["B"]:
+            break
+    v = done / el
+    return {"value": v, "unit": "surfaces/s", "cores": threads, "kind": "oracle",
+            "sample": f"{done} of {w['B']} {w['cfg']['name']} waveforms ({el:.1f} s, float64 direct-sum oracle)"}
+
+
+def run_reference(args, w) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import graf_oracle as O
+    spec = O.LossSpec.from_dict(w["loss"])
+    per_step = {1: 1, 2: 8, 3: 1, 4: 1, 5: 1}[w["cid"]]
+    if w["cid"] == 5:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "float64 direct-sum oracle needs ~10 min per c5 waveform (N=M=16384)"}))
+        return
+
+    def step(i):
+        for j in range(per_step):
+            s = config_waveforms(w["cid"], batch=1, start=(i * per_step + j) % w["B"])[0]
+            O.loss_and_grad(s, w["M"], spec)
+            if w["cfg"]["surface"]:
+                O.surface(s, w["M"], w["cfg"]["surface"], "centered")
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    el = time.perf_counter() - t0
+    v = per_step * args.steps / el
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    line = {"metric": "AF forward+loss+grad surfaces/sec", "value": v, "unit": "surfaces/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": describe(w), "sample_per_step": f"{per_step} waveform(s)"},
+            "cpu_baseline": {"value": v, "unit": "surfaces/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{per_step} waveform(s) per step x {args.steps} steps"},
+            "e2e": {"value": v, "unit": "surfaces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="graf", choices=["graf", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--settle-s", type=float, default=1.0)
+    args = ap.parse_args()
+    w = workload(args.config)
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_22935_b200 as graf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    W = max(3, args.warmup)
+
+    B, N, M = w["B"], w["N"], w["M"]
+    s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=rank * B)).pin_memory()
+    s = s_host.to(dev)
+    spec = graf.LossSpec.from_dict(w["loss"])
+    out = w["cfg"]["surface"]
+    ws = graf.graf.Workspace()
+    grad = torch.empty((B, N), dtype=torch.complex64, device=dev)
+    loss_out = torch.empty((B,), dtype=torch.float64, device=dev)
+    surf = None
+    if out:
+        surf = torch.empty((B, 2 * N - 1, M), dtype=torch.complex64 if out == "c64" else torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def call(st=None):
+        graf.af_loss_grad(s, M, spec, out=out, layout="centered", ws=ws, grad=grad, loss_out=loss_out,
+                          surface=surf, stream=st)
+
+    with torch.cuda.stream(stream):
+        call(stream)                                    # twiddle init + workspace, before capture
+    torch.cuda.synchronize()
+    L = graf.lib()
+    ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
+    ev_k1.record(stream)
+    torch.cuda.synchronize()
+    L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        call(stream)
+    L.graf_set_profile_events(None, None)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            flush.zero_()
+            g.replay()
+        t_end = time.time() + args.settle_s          # bring clocks to load before timing
+        while time.time() < t_end:
+            for _ in range(20):
+                g.replay()
+            stream.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kern_ms = []
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.zero_()
+            ev_a[i].record(stream)
+            g.replay()
+            ev_b[i].record(stream)
+            ev_b[i].synchronize()
+            kern_ms.append(ev_k0.elapsed_time(ev_k1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]
+    total_ms = sum(step_ms)
+    kern_avg = sum(kern_ms) / len(kern_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, kern_avg], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kern_avg = t.tolist()
+    ms_per_step = total_ms / args.steps
+    value = world * B * args.steps / (total_ms / 1e3)
+
+    # ---- e2e: public API, pinned host buffers, H2D + call + D2H inside the timed region
+    g_host = torch.empty((B, N), dtype=torch.complex64).pin_memory()
+    l_host = torch.empty((B,), dtype=torch.float64).pin_memory()
+    s_dev2 = torch.empty_like(s)
+    e2e_ms = []
+    with torch.cuda.stream(stream):
+        for i in range(W + args.steps):
+            flush.zero_()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s_dev2.copy_(s_host, non_blocking=True)
+            lo, gr, _ = graf.af_loss_grad(s_dev2, M, spec, out=out, layout="centered", ws=ws, surface=surf,
+                                          stream=stream)
+            l_host.copy_(lo, non_blocking=True)
+            g_host.copy_(gr, non_blocking=True)
+            b_.record(stream)
+            b_.synchronize()
+            if i >= W:
+                e2e_ms.append(a.elapsed_time(b_))
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = t.item()
+    e2e_value = world * B * len(e2e_ms) / (e2e_total / 1e3)
+
+    # ---- roofline of the dominant kernel (af_rows_kernel), per launch window
+    t_k = kern_avg / 1e3
+    fl_tf = w["flops"] / t_k / 1e12
+    hbm = None
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        hbm = 6650.0
+    bytes_k = w["surf_bytes"] + w["io_bytes"]
+    t_alu = w["flops"] / (FP32_PEAK_TFLOPS * 1e12)
+    t_hbm = bytes_k / (hbm * 1e9)
+    if t_hbm > t_alu:
+        roof = {"bound": "hbm", "achieved": bytes_k / t_k / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": bytes_k / t_k / 1e9 / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    else:
+        roof = {"bound": "alu", "achieved": fl_tf, "peak": round(FP32_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
+                "frac": fl_tf / FP32_PEAK_TFLOPS,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)"}
+    roof["traffic"] = read_traffic(w["cid"])
+    roof["kernel"] = f"af_rows_kernel<{M}> (+ pass-1/reduce when soft-PSL)"
+    roof["kernel_ms"] = kern_avg
+    roof["algorithmic_flops_per_launch"] = w["flops"]
+    roof["algorithmic_bytes_per_launch"] = bytes_k
+    roof["share_of_step"] = kern_avg / ms_per_step
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w)
+    if rank == 0:
+        line = {"metric": "AF forward+loss+grad surfaces/sec", "value": value, "unit": "surfaces/s",
+                "n_gpus": world, "steps": args.steps, "warmup": W, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": describe(w), "B_per_gpu": B, "N": N, "M": M,
+                           "cells_per_s": value * N * M, "parallelism": f"batch-sharded x{world} (weak)",
+                           "l2": "flushed between steps (256 MiB memset, outside the events)",
+                           "timing": "CUDA-graph replay of graf_af_loss_grad per step, CUDA events",
+                           "note": w["note"]},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "surfaces/s", "h2d_bytes_per_step": B * N * 8,
+                        "d2h_bytes_per_step": B * N * 8 + B * 8,
+                        "path": "pinned host s -> H2D -> graf.af_loss_grad (C ABI) -> D2H loss + grad"},
+                "gpu_launches": w["launches"] * args.steps,
+                "clocks": clocks}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_ptr(ev):
+    import ctypes
+    return ctypes.c_void_p(ev.cuda_event)
+
+
+if __name__ == "__main__":
+    main()

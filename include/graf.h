@@ -150,6 +150,13 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
                                   int32_t G, int64_t B, graf_partials* out,
                                   int32_t on_device, void* stream);
 
+/* Diagnostics: with both events non-NULL (cudaEvent_t handles created by the
+ * caller), every later entry-point call made by THIS thread records `start` on
+ * its stream just before its first delay-row kernel (af_rows_kernel) and `stop`
+ * just after its last one, so the caller can time the dominant kernel(s) with
+ * cudaEventElapsedTime (works inside CUDA-graph capture).  (NULL, NULL) = off. */
+graf_status graf_set_profile_events(void* start, void* stop);
+
 #ifdef __cplusplus
 }
 #endif

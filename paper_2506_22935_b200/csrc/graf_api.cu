@@ -17,6 +17,13 @@ namespace graf {
 namespace {
 
 thread_local std::string t_last_error;
+thread_local cudaEvent_t t_prof_start = nullptr, t_prof_stop = nullptr;
+
+cudaError_t prof_mark(bool start, cudaStream_t st) {
+  cudaEvent_t ev = start ? t_prof_start : t_prof_stop;
+  if (!t_prof_start || !t_prof_stop) return cudaSuccess;
+  return cudaEventRecord(ev, st);
+}
 
 graf_status fail(graf_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 graf_status fail(graf_status st, const char* fmt, ...) {
@@ -438,8 +445,10 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
   rp.grad = GRAD_NONE;
   if (loss) fill_loss(rp, af, loss);
   if (pl.U > 0) {
+    prof_mark(true, cs);
     e = launch_rows(pl, rp, (int)af->batch, cs);
     if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (forward) launch");
+    prof_mark(false, cs);
   }
   if (loss) {
     if (pl.U == 0) {
@@ -480,10 +489,13 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   if (loss->lambda_psl == 0.f) {
     rp.grad = GRAD_ISL;  // single fused pass (f' = lambda_isl * w known up front)
     if (pl.U > 0) {
+      prof_mark(true, cs);
       e = launch_rows(pl, rp, (int)af->batch, cs);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (isl) launch");
+      prof_mark(false, cs);
     }
   } else {
+    if (pl.U > 0) prof_mark(true, cs);
     if (!stats) {
       RowParams r1 = rp;
       r1.grad = GRAD_NONE;
@@ -498,6 +510,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     if (pl.U > 0) {
       e = launch_rows(pl, rp, (int)af->batch, cs);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 2) launch");
+      prof_mark(false, cs);
     }
   }
   if (pl.U == 0) {
@@ -527,9 +540,18 @@ graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* 
   rp.mode = MODE_ADJ;
   rp.dA = static_cast<const float2*>(dA);
   rp.grad = GRAD_ADJ;
+  prof_mark(true, cs);
   e = launch_rows(pl, rp, (int)af->batch, cs);
   if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (adjoint) launch");
+  prof_mark(false, cs);
   return run_finalize(af, nullptr, pl, s, ws, nullptr, nullptr, grad, false, cs);
+}
+
+graf_status graf_set_profile_events(void* start, void* stop) {
+  if ((start == nullptr) != (stop == nullptr)) return fail(GRAF_EINVAL, "set both events or neither");
+  t_prof_start = static_cast<cudaEvent_t>(start);
+  t_prof_stop = static_cast<cudaEvent_t>(stop);
+  return GRAF_OK;
 }
 
 graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partials* shards, int32_t G, int64_t B,

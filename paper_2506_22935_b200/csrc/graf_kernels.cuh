@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
   }
   __syncthreads();
   const double Ed = red[0];
-  const float invE = (float)(1.0 / sqrt(Ed));
+  const float invE = (float)(1.0 / Ed);
   const float invE2 = (float)(1.0 / Ed / Ed);
   const float scaleG = p.normalize ? invE2 : 1.0f;
 
