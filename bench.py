@@ -252,15 +252,9 @@ def main():
     with torch.cuda.stream(stream):
         call(stream)                                    # twiddle init + workspace, before capture
     torch.cuda.synchronize()
-    L = graf.lib()
-    ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
-    ev_k1.record(stream)
-    torch.cuda.synchronize()
-    L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         call(stream)
-    L.graf_set_profile_events(None, None)
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
@@ -286,14 +280,27 @@ def main():
             ev_a[i].record(stream)
             g.replay()
             ev_b[i].record(stream)
-            ev_b[i].synchronize()
-            kern_ms.append(ev_k0.elapsed_time(ev_k1))
+        ev_b[-1].synchronize()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]
+    # dominant kernel(s): the ABI records ev_k0/ev_k1 around its delay-row kernels
+    # (graf_set_profile_events); eager calls, same inputs, same L2 flush protocol.
+    L = graf.lib()
+    ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
+    ev_k1.record(stream)
+    torch.cuda.synchronize()
+    L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.zero_()
+            call(stream)
+            ev_k1.synchronize()
+            kern_ms.append(ev_k0.elapsed_time(ev_k1))
+    L.graf_set_profile_events(None, None)
     total_ms = sum(step_ms)
     kern_avg = sum(kern_ms) / len(kern_ms)
     if world > 1:
