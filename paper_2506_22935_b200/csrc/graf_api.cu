@@ -229,43 +229,56 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   return pl;
 }
 
-template <int M>
-cudaError_t launch_rows_t(const Plan& pl, RowParams rp, int B, cudaStream_t st) {
+template <int M, int KIND, bool WGT>
+cudaError_t launch_kernel(const Plan& pl, RowParams rp, int B, cudaStream_t st) {
   static std::once_flag once[kMaxDev];
   static cudaError_t attr_err[kMaxDev];
   int dev = 0;
   cudaGetDevice(&dev);
   std::call_once(once[dev], [dev] {
-    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M, KIND, WGT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err[dev] != cudaSuccess) return attr_err[dev];
   for (int b0 = 0; b0 < B; b0 += 65535) {
     rp.b0 = b0;
     dim3 grid(pl.P, std::min(65535, B - b0));
-    af_rows_kernel<M><<<grid, pl.threads, pl.smem, st>>>(rp);
+    af_rows_kernel<M, KIND, WGT><<<grid, pl.threads, pl.smem, st>>>(rp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-cudaError_t launch_rows(const Plan& pl, const RowParams& rp, int B, cudaStream_t st) {
+template <int M>
+cudaError_t launch_rows_t(const Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind, bool wgt) {
+  switch (kind) {
+    case K_FWD: return wgt ? launch_kernel<M, K_FWD, true>(pl, rp, B, st) : launch_kernel<M, K_FWD, false>(pl, rp, B, st);
+    case K_ISL: return wgt ? launch_kernel<M, K_ISL, true>(pl, rp, B, st) : launch_kernel<M, K_ISL, false>(pl, rp, B, st);
+    case K_PASS2:
+      return wgt ? launch_kernel<M, K_PASS2, true>(pl, rp, B, st) : launch_kernel<M, K_PASS2, false>(pl, rp, B, st);
+    case K_ADJ: return launch_kernel<M, K_ADJ, false>(pl, rp, B, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_rows(const Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind) {
+  const bool wgt = (rp.w_k != nullptr) || (rp.w_d != nullptr);
   switch (pl.M) {
-    case 2: return launch_rows_t<2>(pl, rp, B, st);
-    case 4: return launch_rows_t<4>(pl, rp, B, st);
-    case 8: return launch_rows_t<8>(pl, rp, B, st);
-    case 16: return launch_rows_t<16>(pl, rp, B, st);
-    case 32: return launch_rows_t<32>(pl, rp, B, st);
-    case 64: return launch_rows_t<64>(pl, rp, B, st);
-    case 128: return launch_rows_t<128>(pl, rp, B, st);
-    case 256: return launch_rows_t<256>(pl, rp, B, st);
-    case 512: return launch_rows_t<512>(pl, rp, B, st);
-    case 1024: return launch_rows_t<1024>(pl, rp, B, st);
-    case 2048: return launch_rows_t<2048>(pl, rp, B, st);
-    case 4096: return launch_rows_t<4096>(pl, rp, B, st);
-    case 8192: return launch_rows_t<8192>(pl, rp, B, st);
-    case 16384: return launch_rows_t<16384>(pl, rp, B, st);
+    case 2: return launch_rows_t<2>(pl, rp, B, st, kind, wgt);
+    case 4: return launch_rows_t<4>(pl, rp, B, st, kind, wgt);
+    case 8: return launch_rows_t<8>(pl, rp, B, st, kind, wgt);
+    case 16: return launch_rows_t<16>(pl, rp, B, st, kind, wgt);
+    case 32: return launch_rows_t<32>(pl, rp, B, st, kind, wgt);
+    case 64: return launch_rows_t<64>(pl, rp, B, st, kind, wgt);
+    case 128: return launch_rows_t<128>(pl, rp, B, st, kind, wgt);
+    case 256: return launch_rows_t<256>(pl, rp, B, st, kind, wgt);
+    case 512: return launch_rows_t<512>(pl, rp, B, st, kind, wgt);
+    case 1024: return launch_rows_t<1024>(pl, rp, B, st, kind, wgt);
+    case 2048: return launch_rows_t<2048>(pl, rp, B, st, kind, wgt);
+    case 4096: return launch_rows_t<4096>(pl, rp, B, st, kind, wgt);
+    case 8192: return launch_rows_t<8192>(pl, rp, B, st, kind, wgt);
+    case 16384: return launch_rows_t<16384>(pl, rp, B, st, kind, wgt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -440,13 +453,11 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   RowParams rp = base_params(af, s, pl, ws);
-  rp.mode = MODE_FWD;
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
-  rp.grad = GRAD_NONE;
   if (loss) fill_loss(rp, af, loss);
   if (pl.U > 0) {
     prof_mark(true, cs);
-    e = launch_rows(pl, rp, (int)af->batch, cs);
+    e = launch_rows(pl, rp, (int)af->batch, cs, K_FWD);
     if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (forward) launch");
     prof_mark(false, cs);
   }
@@ -481,16 +492,15 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     // loss from global partials via the finalize path with P partial records absent
   }
   RowParams rp = base_params(af, s, pl, ws);
-  rp.mode = MODE_FWD;
   fill_loss(rp, af, loss);
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
   graf_partials* comb = reinterpret_cast<graf_partials*>(static_cast<char*>(ws) + pl.off_comb);
   const graf_partials* stats = global;
   if (loss->lambda_psl == 0.f) {
-    rp.grad = GRAD_ISL;  // single fused pass (f' = lambda_isl * w known up front)
+    // single fused pass (f' = lambda_isl * w known up front)
     if (pl.U > 0) {
       prof_mark(true, cs);
-      e = launch_rows(pl, rp, (int)af->batch, cs);
+      e = launch_rows(pl, rp, (int)af->batch, cs, K_ISL);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (isl) launch");
       prof_mark(false, cs);
     }
@@ -498,17 +508,15 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     if (pl.U > 0) prof_mark(true, cs);
     if (!stats) {
       RowParams r1 = rp;
-      r1.grad = GRAD_NONE;
       r1.surface = nullptr;
-      e = launch_rows(pl, r1, (int)af->batch, cs);
+      e = launch_rows(pl, r1, (int)af->batch, cs, K_FWD);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 1) launch");
       if ((st = run_partials_reduce(af, loss, pl, ws, comb, cs))) return st;
       stats = comb;
     }
-    rp.grad = GRAD_PASS2;
     rp.stats = stats;
     if (pl.U > 0) {
-      e = launch_rows(pl, rp, (int)af->batch, cs);
+      e = launch_rows(pl, rp, (int)af->batch, cs, K_PASS2);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 2) launch");
       prof_mark(false, cs);
     }
@@ -537,11 +545,9 @@ graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* 
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   RowParams rp = base_params(af, s, pl, ws);
-  rp.mode = MODE_ADJ;
   rp.dA = static_cast<const float2*>(dA);
-  rp.grad = GRAD_ADJ;
   prof_mark(true, cs);
-  e = launch_rows(pl, rp, (int)af->batch, cs);
+  e = launch_rows(pl, rp, (int)af->batch, cs, K_ADJ);
   if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (adjoint) launch");
   prof_mark(false, cs);
   return run_finalize(af, nullptr, pl, s, ws, nullptr, nullptr, grad, false, cs);

@@ -15,6 +15,13 @@
 // final pass lands its outputs in the SAME slots (index t + e*T), so the
 // frequency-domain epilogue and the inverse FFT work in registers with no
 // reordering.  The same slot<->index map holds for time and frequency.
+//
+// Twiddles: the per-thread base twiddle W_M^{(j' mod Ns) M/(Ns R)} of every
+// (pass, q) depends only on the thread, so it is read once per kernel from the
+// correctly rounded table g_tw into registers; the R-1 powers are rebuilt per
+// use by a balanced product tree (depth <= log2 R, error <= ~4 ulp).  When the
+// whole plan has a single twiddled butterfly per thread, all powers stay cached
+// in registers.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -113,40 +120,91 @@ __device__ __forceinline__ void dft(float2* x) {
   }
 }
 
-template <int E>
-struct Log2 {
-  static constexpr int value = E <= 1 ? 0 : 1 + Log2<E / 2>::value;
-};
-template <>
-struct Log2<1> {
-  static constexpr int value = 0;
-};
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
 template <int E>
 __device__ __forceinline__ int padded(int y) {
-  return y + (y >> Log2<E>::value);
+  return y + (y >> ilog2(E));
 }
 
-// One Stockham pass (see header comment).  Non-final passes store to `sh`.
-template <int M, int E, int R, int NS, bool INV, bool LAST>
-__device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t) {
+// ---- compile-time pass plan: radices E, E, ..., remainder
+__host__ __device__ constexpr int pass_radix(int M, int E, int p) {
+  int ns = 1;
+  for (int i = 0; i < p; ++i) ns *= (M / ns >= E ? E : M / ns);
+  return M / ns >= E ? E : M / ns;
+}
+__host__ __device__ constexpr int pass_ns(int M, int E, int p) {
+  int ns = 1;
+  for (int i = 0; i < p; ++i) ns *= pass_radix(M, E, i);
+  return ns;
+}
+__host__ __device__ constexpr int num_passes(int M, int E) {
+  int n = 0;
+  for (int ns = 1; ns < M; ns *= pass_radix(M, E, n), ++n) {
+  }
+  return n;
+}
+// register slots of base twiddles before pass p (passes >= 1 have twiddles)
+__host__ __device__ constexpr int tw_offset(int M, int E, int p) {
+  int off = 0;
+  for (int i = 1; i < p; ++i) off += E / pass_radix(M, E, i);
+  return off;
+}
+
+template <int R>
+__device__ __forceinline__ void tw_powers(float2 w1, float2* w) {
+  w[0] = make_float2(1.f, 0.f);
+  if constexpr (R > 1) w[1] = w1;
+#pragma unroll
+  for (int r = 2; r < R; ++r) w[r] = cmul(w[r / 2], w[r - r / 2]);
+}
+
+template <int M, int E>
+struct Twiddles {
+  static constexpr int T = M / E;
+  static constexpr int NP = num_passes(M, E);
+  static constexpr int NB = tw_offset(M, E, NP);          // base twiddles per thread
+  static constexpr bool CACHE = (NB == 1);                // single twiddled butterfly: keep all powers
+  static constexpr int RC = CACHE ? pass_radix(M, E, 1) : 1;
+  float2 base[NB > 0 ? NB : 1];
+  float2 pw[RC];
+
+  __device__ __forceinline__ void init(int t) {
+#pragma unroll
+    for (int p = 1; p < NP; ++p) {
+      const int ns = pass_ns(M, E, p), R = pass_radix(M, E, p), Q = E / R;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int jm = (t + q * T) & (ns - 1);
+        base[tw_offset(M, E, p) + q] = g_tw[(jm * (M / (ns * R))) * (kMaxM / M)];
+      }
+    }
+    if constexpr (CACHE) tw_powers<RC>(base[0], pw);
+  }
+};
+
+// One Stockham pass P (see header comment).  Non-final passes store to `sh`.
+template <int M, int E, int P, bool INV>
+__device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t, const Twiddles<M, E>& tw) {
   constexpr int T = M / E;
+  constexpr int R = pass_radix(M, E, P);
+  constexpr int NS = pass_ns(M, E, P);
   constexpr int Q = E / R;
-  constexpr int TWS = kMaxM / M;
+  constexpr bool LAST = (NS * R == M);
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     float2 x[R];
-    const int jp = t + q * T;
-    const int jm = jp & (NS - 1);
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[q + r * Q];
     if constexpr (NS > 1) {
-      const int step = jm * (M / (NS * R));
+      if constexpr (Twiddles<M, E>::CACHE) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        float2 w = g_tw[((step * r) & (M - 1)) * TWS];
-        if (INV) w.y = -w.y;
-        x[r] = cmul(x[r], w);
+        for (int r = 1; r < R; ++r) x[r] = INV ? cmulc(x[r], tw.pw[r]) : cmul(x[r], tw.pw[r]);
+      } else {
+        float2 w[R];
+        tw_powers<R>(tw.base[tw_offset(M, E, P) + q], w);
+#pragma unroll
+        for (int r = 1; r < R; ++r) x[r] = INV ? cmulc(x[r], w[r]) : cmul(x[r], w[r]);
       }
     }
     dft<R, INV>(x);
@@ -154,6 +212,8 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t)
 #pragma unroll
       for (int r = 0; r < R; ++r) v[q + r * Q] = x[r];
     } else {
+      const int jp = t + q * T;
+      const int jm = jp & (NS - 1);
       const int base = (jp / NS) * NS * R + jm;
 #pragma unroll
       for (int r = 0; r < R; ++r) sh[padded<E>(base + r * NS)] = x[r];
@@ -161,21 +221,20 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t)
   }
 }
 
-// Full length-M FFT on the register slots of one row slot.  SYNC() orders the
+// Full length-M FFT on the register slots of one row slot.  sync() orders the
 // row slot's shared-memory exchange (warp sync, named barrier or CTA barrier).
-template <int M, int E, int NS, bool INV, class Sync>
-__device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, const Sync& sync) {
+template <int M, int E, int P, bool INV, class Sync>
+__device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, const Twiddles<M, E>& tw,
+                                         const Sync& sync) {
   constexpr int T = M / E;
-  constexpr int REM = M / NS;
-  constexpr int R = REM >= E ? E : REM;
-  constexpr bool LAST = (NS * R == M);
-  stockham_pass<M, E, R, NS, INV, LAST>(v, sh, t);
-  if constexpr (!LAST) {
+  constexpr int NP = num_passes(M, E);
+  stockham_pass<M, E, P, INV>(v, sh, t, tw);
+  if constexpr (P + 1 < NP) {
     sync();
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
     sync();
-    fft_rows<M, E, NS * R, INV, Sync>(v, sh, t, sync);
+    fft_rows<M, E, P + 1, INV, Sync>(v, sh, t, tw, sync);
   }
 }
 

@@ -1,6 +1,6 @@
 // graf_kernels.cuh — the delay-row kernel and the reductions of the GRAF hot path.
 //
-// One kernel template, `af_rows_kernel<M>`, covers SURVEY.md §8(a) rows a0-a7:
+// One kernel template, `af_rows_kernel<M, KIND, WGT>`, covers SURVEY.md §8(a) rows a0-a7:
 //   a0  stage s[b] in shared memory, energy E_b (double, fixed order)
 //   a1  lag product r_k[n] = s[n] conj(s[n-k]) straight into the FFT registers
 //       (Eqs. 8-10; the shift matrix S of Eq. 9 is never built)
@@ -11,18 +11,21 @@
 //   a5  cotangent G = f' A / E^2 (Eq. 14)
 //   a6  inverse Doppler FFT H = M*IFFT(G) (L230)
 //   a7  delay correlation g[p] += H[k,p] s[p-k] + conj(H[k,p+k]) s[p+k] (Eq. 15)
+// KIND selects the pass at compile time:
+//   K_FWD   a0-a3F/a3L            (graf_af_forward; pass 1 of soft-PSL)
+//   K_ISL   a0-a7 in ONE pass      (ISL-only losses: f' = lambda_isl*w is known up front)
+//   K_PASS2 a0-a7 with f' from the combined pass-1 partials (soft-PSL)
+//   K_ADJ   dA row -> a6-a7        (graf_af_backward, unfolded rows)
 // Rows are folded to k >= 0 (symmetric masks/weights): row k > 0 stands for
 // rows +k and -k (loss sums and gradient terms counted twice; SURVEY §8(c)
-// "symmetric-loss identities").  The generic adjoint (graf_af_backward) runs
-// the same kernel in MODE_ADJ on unfolded rows read from dA.
+// "symmetric-loss identities").
 #pragma once
-#include "graf_fft.cuh"
 #include "../../include/graf.h"
+#include "graf_fft.cuh"
 
 namespace graf {
 
-enum : int { MODE_FWD = 0, MODE_ADJ = 1 };
-enum : int { GRAD_NONE = 0, GRAD_ISL = 1, GRAD_PASS2 = 2, GRAD_ADJ = 3 };
+enum : int { K_FWD = 0, K_ISL = 1, K_PASS2 = 2, K_ADJ = 3 };
 constexpr int kPart = 8;  // doubles per CTA partial record: S, max, Z, C, fchi, -, -, -
 
 struct RowParams {
@@ -30,7 +33,6 @@ struct RowParams {
   int N, B, b0;      // b0: first waveform of this launch (grid.y chunking)
   int U;             // rows enumerated per waveform
   int row_lo, row_step;
-  int mode;          // MODE_FWD (lag products, folded rows) | MODE_ADJ (rows from dA, unfolded)
   // surface window / dA rows
   int kb, ke;
   void* surface;
@@ -47,8 +49,7 @@ struct RowParams {
   int centred;
   float xbar;
   double omega;        // |Omega| (full region, for the centred mean)
-  int grad;            // GRAD_*
-  const graf_partials* stats;  // combined partials [B] for GRAD_PASS2
+  const graf_partials* stats;  // combined partials [B] for K_PASS2
   // outputs
   double* part;        // [B][P][kPart]
   float2* gpart;       // [B][P][N]
@@ -109,14 +110,50 @@ __device__ __forceinline__ double warp_energy(const float2* sb, int N, int lane)
   return acc;  // valid in lane 0
 }
 
-struct LsePart {
-  double S, Z, C, F;
-  float mx;
-};
+// Deterministic CTA reductions (fixed shuffle tree, fixed warp order); result in thread 0.
+template <int THREADS>
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  constexpr int NW = (THREADS + 31) / 32;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if constexpr (NW == 1) {
+    return v;
+  } else {
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0)
+      for (int w = 0; w < NW; ++w) r += scratch[w];
+    __syncthreads();
+    return r;
+  }
+}
+
+template <int THREADS>
+__device__ __forceinline__ float block_max_all(float v, double* scratch) {
+  constexpr int NW = (THREADS + 31) / 32;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+  if constexpr (NW == 1) {
+    return v;
+  } else {
+    float* sc = reinterpret_cast<float*>(scratch);
+    if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = v;
+    __syncthreads();
+    float r = -INFINITY;
+    for (int w = 0; w < NW; ++w) r = fmaxf(r, sc[w]);
+    __syncthreads();
+    return r;  // in every thread
+  }
+}
 
 __device__ __forceinline__ void lse_merge(float& m, double& Z, float m2, double Z2, float invT) {
   if (m2 == -INFINITY) return;
-  if (m == -INFINITY) { m = m2; Z = Z2; return; }
+  if (m == -INFINITY) {
+    m = m2;
+    Z = Z2;
+    return;
+  }
   if (m2 > m) {
     Z = Z * exp((double)(m - m2) * invT) + Z2;
     m = m2;
@@ -125,10 +162,14 @@ __device__ __forceinline__ void lse_merge(float& m, double& Z, float m2, double 
   }
 }
 
-template <int M>
+// float exp(x) for x <= 0 through the MUFU ex2 unit (rel. error ~2 ulp)
+__device__ __forceinline__ float exp_fast(float x) { return exp2f(x * 1.4426950408889634f); }
+
+template <int M, int KIND, bool WGT>
 __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
+  constexpr bool GRAD = (KIND != K_FWD);
   extern __shared__ float4 smem_raw[];
   float2* smem = reinterpret_cast<float2*>(smem_raw);
 
@@ -139,21 +180,19 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float2* sg = p.s + (size_t)b * N;
 
-  // ---- shared-memory carve-up: [energy scratch][s][exchange x S][g x S]
-  double* red = reinterpret_cast<double*>(smem);  // 64 doubles of scratch
+  // ---- shared-memory carve-up: [scratch 64 doubles][s][exchange x S][g x S]
+  double* red = reinterpret_cast<double*>(smem);
   float2* s_sh = smem + 64;
   float2* xch = s_sh + (C::S_SMEM ? ((N + 1) & ~1) : 0);
   float2* gacc_sh = xch + S * XS;
   const float2* sv = C::S_SMEM ? s_sh : sg;
-  const bool want_g = (p.grad != GRAD_NONE);
-  float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * N
-                           : p.gpart + ((size_t)b * P + pb) * N;  // S == 1 when !G_SMEM
+  float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * N : p.gpart + ((size_t)b * P + pb) * N;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
   if constexpr (C::S_SMEM) {
     for (int i = threadIdx.x; i < N; i += THREADS) s_sh[i] = sg[i];
   }
-  if (want_g) {
+  if constexpr (GRAD) {
     if constexpr (C::G_SMEM) {
       for (int i = threadIdx.x; i < S * N; i += THREADS) gacc_sh[i] = make_float2(0.f, 0.f);
     } else {
@@ -164,6 +203,18 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
     const double e = warp_energy(sg, N, lane);
     if (lane == 0) red[0] = e;
   }
+  Twiddles<M, E> tw;
+  tw.init(t);
+  // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
+  unsigned band = 0u, mlb = 0u;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int m = t + e * T;
+    const int d = m < M / 2 ? m : m - M;
+    const int ad = d < 0 ? -d : d;
+    band |= (ad <= p.d_max ? 1u : 0u) << e;
+    mlb |= (ad <= p.ml_d ? 1u : 0u) << e;
+  }
   __syncthreads();
   const double Ed = red[0];
   const float invE = (float)(1.0 / Ed);
@@ -173,10 +224,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
   // pass-2 statistics from the combined partials (reading R13)
   float lse = 0.f, ebar = 0.f, invZc = 0.f;
   bool use_centred = false;
-  if (p.grad == GRAD_PASS2) {
+  if constexpr (KIND == K_PASS2) {
     const graf_partials g = p.stats[b];
-    const double lse_d = g.lse_max + (double)p.T * log(g.lse_sum);
-    lse = (float)lse_d;
+    lse = (float)(g.lse_max + (double)p.T * log(g.lse_sum));
     if (p.centred) {
       const double zc = p.omega + g.cen_sum;
       use_centred = isfinite(zc) && (g.lse_max - p.xbar) * p.invT <= 40.0;
@@ -184,6 +234,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
       invZc = (float)(1.0 / zc);
     }
   }
+  const bool want_lse = (KIND == K_FWD) && p.loss_on && p.lam_psl != 0.f;
 
   SlotSync<T, S> sync{1 + slot};
   float2* sh = xch + (size_t)slot * XS;
@@ -200,17 +251,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
     const int u = it * rows_per_iter + pb * S + slot;
     const bool valid = u < p.U;
     const int k = p.row_lo + (valid ? u : 0) * p.row_step;
-    float2 v[E];
-
-    bool lrow = false, wpos = false, wneg = false;
-    float mult = 1.f;
     const int lo = k > 0 ? k : 0;
     const int hi = k < 0 ? N + k : N;
+    float2 v[E];
+    bool lrow;
+    float mult;
 
-    if (p.mode == MODE_FWD) {
+    if constexpr (KIND != K_ADJ) {
       // ---- a1: lag product into the first-pass registers (time index n = t + e*T)
-      wpos = valid && p.surface && k >= p.kb && k < p.ke;
-      wneg = valid && p.surface && k > 0 && -k >= p.kb && -k < p.ke;
+      const bool wpos = valid && p.surface && k >= p.kb && k < p.ke;
+      const bool wneg = valid && p.surface && k > 0 && -k >= p.kb && -k < p.ke;
       lrow = valid && p.loss_on && k <= p.kloss && (k % p.shard_count) == p.shard_index;
       mult = (k == 0) ? 1.f : 2.f;
 #pragma unroll
@@ -221,210 +271,184 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
         v[e] = r;
       }
       // ---- a2: forward Doppler FFT
-      fft_rows<M, E, 1, false>(v, sh, t, sync);
+      fft_rows<M, E, 0, false>(v, sh, t, tw, sync);
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
       if (wpos || wneg) {
         const float nrm = p.norm_out ? invE : 1.f;
+        const int lay = p.layout ? M / 2 : 0;
+        if (p.out_kind == GRAF_OUT_C64) {
+          float2* out = reinterpret_cast<float2*>(p.surface);
+          float2* rp = out + ((size_t)b * surf_rows + (k - p.kb)) * M;
+          float2* rn = out + ((size_t)b * surf_rows + (-k - p.kb)) * M;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int m = t + e * T;
-          const float2 A = v[e];
-          if (p.out_kind == GRAF_OUT_C64) {
-            float2* out = reinterpret_cast<float2*>(p.surface);
-            if (wpos) {
-              const int col = p.layout ? ((m + M / 2) & (M - 1)) : m;
-              __stcs(out + ((size_t)b * surf_rows + (k - p.kb)) * M + col, cscale(A, nrm));
-            }
+          for (int e = 0; e < E; ++e) {
+            const int m = t + e * T;
+            if (wpos) __stcs(rp + ((m + lay) & (M - 1)), cscale(v[e], nrm));
             if (wneg) {
               const int mn = (M - m) & (M - 1);
-              const int col = p.layout ? ((mn + M / 2) & (M - 1)) : mn;
+              // A[-k, mn] = e^{+2 pi i mn k / M} conj(A[k, m]) = conj(W^{mn k} A)
               const float2 w = g_tw[(int)(((long long)mn * k) & (M - 1)) * (kMaxM / M)];
-              // A[-k, mn] = e^{+2 pi i mn k / M} conj(A[k, m]) = conj(w) * conj(A)
-              const float2 val = cconj(cmul(w, A));
-              __stcs(out + ((size_t)b * surf_rows + (-k - p.kb)) * M + col, cscale(val, nrm));
+              __stcs(rn + ((mn + lay) & (M - 1)), cscale(cconj(cmul(w, v[e])), nrm));
             }
-          } else {
-            float* out = reinterpret_cast<float*>(p.surface);
-            const float chi = A.x * A.x + A.y * A.y;
-            const float val = (p.out_kind == GRAF_OUT_ABS_F32) ? sqrtf(chi) * nrm : chi * nrm * nrm;
-            if (wpos) {
-              const int col = p.layout ? ((m + M / 2) & (M - 1)) : m;
-              __stcs(out + ((size_t)b * surf_rows + (k - p.kb)) * M + col, val);
-            }
-            if (wneg) {
-              const int mn = (M - m) & (M - 1);
-              const int col = p.layout ? ((mn + M / 2) & (M - 1)) : mn;
-              __stcs(out + ((size_t)b * surf_rows + (-k - p.kb)) * M + col, val);
-            }
+          }
+        } else {
+          float* out = reinterpret_cast<float*>(p.surface);
+          float* rp = out + ((size_t)b * surf_rows + (k - p.kb)) * M;
+          float* rn = out + ((size_t)b * surf_rows + (-k - p.kb)) * M;
+          const bool absk = p.out_kind == GRAF_OUT_ABS_F32;
+          const float sc = absk ? nrm : nrm * nrm;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int m = t + e * T;
+            const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+            const float val = (absk ? sqrtf(chi) : chi) * sc;
+            if (wpos) __stcs(rp + ((m + lay) & (M - 1)), val);
+            if (wneg) __stcs(rn + (((M - m) + lay) & (M - 1)), val);
           }
         }
       }
 
       // ---- a3L (+ a5): loss partials and the cotangent
       if (lrow) {
-        const float wk = p.w_k ? p.w_k[k + N - 1] : 1.f;
-        float rowS = 0.f, rowM = -INFINITY;
-        unsigned inmask = 0u;
+        const unsigned inm = band & ~(k <= p.ml_k ? mlb : 0u);
+        const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
+        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const int m = t + e * T;
-          const int d = m < M / 2 ? m : m - M;
-          const int ad = d < 0 ? -d : d;
-          const bool in = ad <= p.d_max && !(k <= p.ml_k && ad <= p.ml_d);
-          if (in) {
-            inmask |= 1u << e;
-            const float w = wk * (p.w_d ? p.w_d[d + M / 2] : 1.f);
-            const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-            rowS = fmaf(w, chi, rowS);
-            const float x = p.normalize ? chi * invE2 : chi;
-            rowM = fmaxf(rowM, x);
-          }
-        }
-        accS += (double)mult * rowS;
-        if (p.lam_psl != 0.f && p.grad != GRAD_PASS2 && inmask) {
-          if (rowM > accM) {
-            accZ = (accM == -INFINITY) ? 0.0 : accZ * exp((double)(accM - rowM) * p.invT);
-            accM = rowM;
-          }
-          float rowZ = 0.f, rowC = 0.f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            if (inmask & (1u << e)) {
-              const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-              const float x = p.normalize ? chi * invE2 : chi;
-              rowZ += __expf((x - accM) * p.invT);
-              if (p.centred) rowC += expm1f((x - p.xbar) * p.invT);
-            }
-          }
-          accZ += (double)mult * rowZ;
-          accC += (double)mult * rowC;
-        } else if (p.lam_psl == 0.f && inmask) {
-          accM = fmaxf(accM, rowM);
-        }
-        if (p.grad == GRAD_ISL || p.grad == GRAD_PASS2) {
-          float rowF = 0.f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            float2 G = make_float2(0.f, 0.f);
-            if (inmask & (1u << e)) {
+          if (inm & (1u << e)) {
+            float w = 1.f;
+            if constexpr (WGT) {
               const int m = t + e * T;
               const int d = m < M / 2 ? m : m - M;
-              const float w = wk * (p.w_d ? p.w_d[d + M / 2] : 1.f);
-              const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+              w = wk * (p.w_d ? p.w_d[d + M / 2] : 1.f);
+            }
+            const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+            rowS = fmaf(w, chi, rowS);
+            if constexpr (KIND == K_FWD) {
+              rowM = fmaxf(rowM, p.normalize ? chi * invE2 : chi);
+            } else {
               float fp;
-              if (p.grad == GRAD_ISL) {
+              if constexpr (KIND == K_ISL) {
                 fp = p.lam_isl * w;
               } else {
                 const float x = p.normalize ? chi * invE2 : chi;
                 if (use_centred) {
                   fp = p.lam_psl * (expm1f((x - p.xbar) * p.invT) - ebar) * invZc;
                 } else {
-                  fp = p.lam_isl * w + p.lam_psl * __expf((x - lse) * p.invT);
+                  fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);
                 }
               }
               rowF = fmaf(fp, chi, rowF);
-              G = cscale(v[e], fp * scaleG);
+              v[e] = cscale(v[e], fp * scaleG * mult);   // G (x2 for a folded row pair)
             }
-            v[e] = G;
+          } else if constexpr (GRAD) {
+            v[e] = make_float2(0.f, 0.f);
           }
-          accF += (double)mult * rowF;
         }
+        accS += (double)(mult * rowS);
+        accF += (double)(mult * rowF);
+        if constexpr (KIND == K_FWD) {
+          if (want_lse && rowM > -INFINITY) {
+            if (rowM > accM) {
+              accZ = (accM == -INFINITY) ? 0.0 : accZ * (double)exp_fast((accM - rowM) * p.invT);
+              accM = rowM;
+            }
+            float rowZ = 0.f, rowC = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              if (inm & (1u << e)) {
+                const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+                const float x = p.normalize ? chi * invE2 : chi;
+                rowZ += exp_fast((x - accM) * p.invT);
+                if (p.centred) rowC += expm1f((x - p.xbar) * p.invT);
+              }
+            }
+            accZ += (double)(mult * rowZ);
+            accC += (double)(mult * rowC);
+          } else {
+            accM = fmaxf(accM, rowM);
+          }
+        }
+      } else if constexpr (GRAD) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
       }
     } else {
-      // ---- MODE_ADJ: G = dA row (unfolded k = kb + u)
+      // ---- K_ADJ: G = dA row (unfolded k = kb + u)
       lrow = valid;
       mult = 1.f;
       const float2* drow = p.dA + ((size_t)b * surf_rows + (k - p.kb)) * M;
+      const int lay = p.layout ? M / 2 : 0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int m = t + e * T;
-        const int col = p.layout ? ((m + M / 2) & (M - 1)) : m;
-        v[e] = valid ? __ldcs(drow + col) : make_float2(0.f, 0.f);
+        v[e] = valid ? __ldcs(drow + ((m + lay) & (M - 1))) : make_float2(0.f, 0.f);
       }
     }
 
     // ---- a6 + a7: inverse Doppler FFT and the delay correlation
-    bool do_adj = want_g && p.grad != GRAD_NONE && lrow;
-    if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
-    if (do_adj) {
-      if (!lrow) {
+    if constexpr (GRAD) {
+      bool do_adj = lrow;
+      if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
+      if (do_adj) {
+        fft_rows<M, E, 0, true>(v, sh, t, tw, sync);
+        if (lrow) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
-      }
-      fft_rows<M, E, 1, true>(v, sh, t, sync);
-      if (lrow) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int n = t + e * T;
-          if (n >= lo && n < hi) {
-            const float2 add = cscale(cmul(v[e], sv[n - k]), mult);  // term 1 at p = n
-            gacc[n] = cadd(gacc[n], add);
+          for (int e = 0; e < E; ++e) {
+            const int n = t + e * T;
+            if (n >= lo && n < hi) gacc[n] = cadd(gacc[n], cmul(v[e], sv[n - k]));  // term 1 at p = n
           }
         }
-      }
-      sync();
-      if (lrow) {
+        sync();
+        if (lrow) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int n = t + e * T;
-          if (n >= lo && n < hi) {
-            const float2 add = cscale(cmul(cconj(v[e]), sv[n]), mult);  // term 2 at p = n - k
-            gacc[n - k] = cadd(gacc[n - k], add);
+          for (int e = 0; e < E; ++e) {
+            const int n = t + e * T;
+            if (n >= lo && n < hi) gacc[n - k] = cadd(gacc[n - k], cmulc(sv[n], v[e]));  // term 2 at p = n-k
           }
         }
+        sync();
       }
-      sync();
     }
   }
 
-  // ---- CTA reduction of the scalar partials (fixed shuffle tree + fixed warp order)
+  // ---- CTA reduction of the scalar partials -> part[b][pb]
   __syncthreads();
-  {
-    double vS = accS, vZ = accZ, vC = accC, vF = accF;
-    float vM = accM;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double oS = __shfl_down_sync(0xffffffffu, vS, off);
-      const double oZ = __shfl_down_sync(0xffffffffu, vZ, off);
-      const double oC = __shfl_down_sync(0xffffffffu, vC, off);
-      const double oF = __shfl_down_sync(0xffffffffu, vF, off);
-      const float oM = __shfl_down_sync(0xffffffffu, vM, off);
-      if (lane + off < 32) {
-        vS += oS; vC += oC; vF += oF;
-        lse_merge(vM, vZ, oM, oZ, p.invT);
+  double* scratch = reinterpret_cast<double*>(xch);  // exchange space is free now
+  double* rec = p.part + ((size_t)b * P + pb) * kPart;
+  if constexpr (KIND != K_ADJ) {
+    const double S0 = block_sum<THREADS>(accS, scratch);
+    const double F0 = block_sum<THREADS>(accF, scratch);
+    double Z0 = 0.0, C0 = 0.0;
+    float M0 = -INFINITY;
+    if constexpr (KIND == K_FWD) {
+      M0 = block_max_all<THREADS>(accM, scratch);
+      if (want_lse) {
+        const double zs = (accM == -INFINITY) ? 0.0 : accZ * (double)exp_fast((accM - M0) * p.invT);
+        Z0 = block_sum<THREADS>(zs, scratch);
+        C0 = block_sum<THREADS>(accC, scratch);
       }
     }
-    double* wred = reinterpret_cast<double*>(xch);  // reuse exchange space
-    constexpr int NW = (THREADS + 31) / 32;
-    if (lane == 0) {
-      wred[warp * 5 + 0] = vS;
-      wred[warp * 5 + 1] = vZ;
-      wred[warp * 5 + 2] = vC;
-      wred[warp * 5 + 3] = vF;
-      wred[warp * 5 + 4] = (double)vM;
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
-      double S0 = 0, Z0 = 0, C0 = 0, F0 = 0;
-      float M0 = -INFINITY;
-      for (int w = 0; w < NW; ++w) {
-        S0 += wred[w * 5 + 0];
-        C0 += wred[w * 5 + 2];
-        F0 += wred[w * 5 + 3];
-        lse_merge(M0, Z0, (float)wred[w * 5 + 4], wred[w * 5 + 1], p.invT);
-      }
-      double* rec = p.part + ((size_t)b * P + pb) * kPart;
       rec[0] = S0;
       rec[1] = (double)M0;
       rec[2] = Z0;
       rec[3] = C0;
       rec[4] = F0;
     }
+  } else {
+    if (threadIdx.x == 0) {
+      rec[0] = 0.0;
+      rec[1] = -INFINITY;
+      rec[2] = 0.0;
+      rec[3] = 0.0;
+      rec[4] = 0.0;
+    }
   }
 
   // ---- gradient accumulators of all slots -> this CTA's partial g (fixed slot order)
-  if (want_g && C::G_SMEM) {
+  if constexpr (GRAD && C::G_SMEM) {
     float2* gout = p.gpart + ((size_t)b * P + pb) * N;
     for (int n = threadIdx.x; n < N; n += THREADS) {
       float2 a = gacc_sh[n];
@@ -436,14 +460,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: combine the P CTA partial records of each waveform -> graf_partials[B]
-// (+ the loss when `loss_out` != NULL).  One thread per waveform, fixed order.
+// K3: combine the P CTA partial records of each waveform -> graf_partials[B].
+// One thread per waveform, fixed order.
 // ---------------------------------------------------------------------------
 struct ReduceParams {
   const double* part;
   int P, B;
   float invT, T;
-  graf_partials* out;   // may be NULL
+  graf_partials* out;
 };
 
 __global__ void partials_reduce_kernel(ReduceParams r) {
