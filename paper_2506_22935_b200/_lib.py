@@ -7,7 +7,8 @@ import os
 from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_size_t, c_void_p, c_char_p
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgraf.so")
+# GRAF_LIB_PATH: tuning builds only (scripts/tune.py); the default is the in-tree library.
+LIB_PATH = os.environ.get("GRAF_LIB_PATH") or os.path.join(PKG, "libgraf.so")
 
 ABI_VERSION = 1
 GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_ENONFINITE, GRAF_EWORKSPACE = range(6)

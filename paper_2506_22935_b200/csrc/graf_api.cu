@@ -68,8 +68,9 @@ cudaError_t ensure_twiddles() {
 // launch plan
 // ---------------------------------------------------------------------------
 struct Plan {
-  int M = 0, threads = 0, S = 0, T = 0, P = 1;
+  int M = 0, threads = 0, S = 0, T = 0, P = 1, Pbound = 1;
   int U = 0, row_lo = 0, row_step = 1;
+  bool fixedP = false;
   bool s_smem = true, g_smem = true;
   size_t smem = 0;
   size_t off_part = 0, off_gpart = 0, off_comb = 0, total = 0;
@@ -210,36 +211,71 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   }
   pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? (size_t)ci.S * N : 0));
-  int occ = std::min(2048 / ci.threads, 32);
-  occ = std::max(1, std::min<int>(occ, (int)((228 * 1024) / (pl.smem + 1024))));
-  const long long target = (long long)kNumSM * occ * 4;
+  // Upper bound on CTAs per waveform (sizes the workspace); the launch picks the
+  // actual P <= bound from the kernel's measured occupancy (choose_P).
   const long long B = af->batch;
-  long long P = (target + B - 1) / B;
   const long long maxP = std::max(1, (pl.U + ci.S - 1) / ci.S);
-  P = std::max(1LL, std::min(P, maxP));
-  pl.P = (int)P;
+  const long long capP = std::max(1LL, (long long)(kNumSM * 8 + B - 1) / B);
+  pl.P = (int)std::max(1LL, std::min(maxP, capP));
+  pl.Pbound = pl.P;
   size_t off = 0;
   pl.off_part = off;
-  off = align256(off + sizeof(double) * kPart * (size_t)B * pl.P);
+  off = align256(off + sizeof(double) * kPart * (size_t)B * pl.Pbound);
   pl.off_gpart = off;
-  if (grad) off = align256(off + sizeof(float2) * (size_t)B * pl.P * N);
+  if (grad) off = align256(off + sizeof(float2) * (size_t)B * pl.Pbound * N);
   pl.off_comb = off;
   off = align256(off + sizeof(graf_partials) * (size_t)B);
   pl.total = off;
   return pl;
 }
 
+// Cost model: waves x (row iterations + CTA setup), setup ~ one row iteration.
+int choose_P(const Plan& pl, long long B, int occ, int nsm) {
+  const long long cap = (long long)nsm * std::max(occ, 1);
+  int best = 1;
+  double best_t = 1e300;
+  for (int P = 1; P <= pl.Pbound; ++P) {
+    const long long ctas = (long long)P * B;
+    const double waves = (double)((ctas + cap - 1) / cap);
+    const double iters = (double)((pl.U + (long long)P * pl.S - 1) / ((long long)P * pl.S));
+    const double t = waves * (iters + 1.0);
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = P;
+    }
+  }
+  return best;
+}
+
 template <int M, int KIND, bool WGT>
-cudaError_t launch_kernel(const Plan& pl, RowParams rp, int B, cudaStream_t st) {
+cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
   static std::once_flag once[kMaxDev];
   static cudaError_t attr_err[kMaxDev];
+  static int sm_count[kMaxDev];
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::call_once(once[dev], [dev] {
     attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M, KIND, WGT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (attr_err[dev] == cudaSuccess)
+      attr_err[dev] = cudaDeviceGetAttribute(&sm_count[dev], cudaDevAttrMultiProcessorCount, dev);
   });
   if (attr_err[dev] != cudaSuccess) return attr_err[dev];
+  *nsm = sm_count[dev];
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT>, Cfg<M>::THREADS, smem);
+}
+
+template <int M, int KIND, bool WGT>
+cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
+  if (!pl.fixedP) {
+    int occ = 1, nsm = kNumSM;
+    cudaError_t e = kernel_occupancy<M, KIND, WGT>(pl.smem, &occ, &nsm);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    pl.P = choose_P(pl, B, occ, nsm);
+    pl.fixedP = true;   // later passes of the same call reuse it
+  }
   for (int b0 = 0; b0 < B; b0 += 65535) {
     rp.b0 = b0;
     dim3 grid(pl.P, std::min(65535, B - b0));
@@ -251,7 +287,7 @@ cudaError_t launch_kernel(const Plan& pl, RowParams rp, int B, cudaStream_t st) 
 }
 
 template <int M>
-cudaError_t launch_rows_t(const Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind, bool wgt) {
+cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind, bool wgt) {
   switch (kind) {
     case K_FWD: return wgt ? launch_kernel<M, K_FWD, true>(pl, rp, B, st) : launch_kernel<M, K_FWD, false>(pl, rp, B, st);
     case K_ISL: return wgt ? launch_kernel<M, K_ISL, true>(pl, rp, B, st) : launch_kernel<M, K_ISL, false>(pl, rp, B, st);
@@ -262,8 +298,12 @@ cudaError_t launch_rows_t(const Plan& pl, const RowParams& rp, int B, cudaStream
   }
 }
 
-cudaError_t launch_rows(const Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind) {
+cudaError_t launch_rows(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind) {
   const bool wgt = (rp.w_k != nullptr) || (rp.w_d != nullptr);
+#ifdef GRAF_ONLY_M  // tuning builds (scripts/tune.py) instantiate a single size
+  if (pl.M == GRAF_ONLY_M) return launch_rows_t<GRAF_ONLY_M>(pl, rp, B, st, kind, wgt);
+  return cudaErrorNotSupported;
+#else
   switch (pl.M) {
     case 2: return launch_rows_t<2>(pl, rp, B, st, kind, wgt);
     case 4: return launch_rows_t<4>(pl, rp, B, st, kind, wgt);
@@ -281,6 +321,7 @@ cudaError_t launch_rows(const Plan& pl, const RowParams& rp, int B, cudaStream_t
     case 16384: return launch_rows_t<16384>(pl, rp, B, st, kind, wgt);
     default: return cudaErrorInvalidValue;
   }
+#endif
 }
 
 void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
@@ -447,7 +488,7 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
   graf_status st = common_checks(af, loss, s, surface, false);
   if (st) return st;
   if (loss && !partials) return fail(GRAF_EINVAL, "loss given but partials is NULL");
-  const Plan pl = make_plan(af, loss, Kind::Forward);
+  Plan pl = make_plan(af, loss, Kind::Forward);
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
@@ -480,7 +521,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   if (!loss) return fail(GRAF_EINVAL, "loss descriptor is NULL");
   if (!grad) return fail(GRAF_EINVAL, "grad is NULL");
   if (!aligned8(grad)) return fail(GRAF_EINVAL, "grad is not 8-byte aligned");
-  const Plan pl = make_plan(af, loss, Kind::LossGrad);
+  Plan pl = make_plan(af, loss, Kind::LossGrad);
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
@@ -539,7 +580,7 @@ graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* 
   if (st) return st;
   if (!dA || !aligned8(dA)) return fail(GRAF_EINVAL, "dA is NULL or not 8-byte aligned");
   if (!grad || !aligned8(grad)) return fail(GRAF_EINVAL, "grad is NULL or not 8-byte aligned");
-  const Plan pl = make_plan(af, nullptr, Kind::Backward);
+  Plan pl = make_plan(af, nullptr, Kind::Backward);
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();

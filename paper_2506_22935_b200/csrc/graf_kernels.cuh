@@ -67,20 +67,72 @@ struct Cfg;
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
     static constexpr bool G_SMEM = (M_ <= 8192);                     \
   };
+// Defaults; a tuning build may override one size with -DGRAF_E_<M>=.. -DGRAF_S_<M>=..
+#ifndef GRAF_E_64
+#define GRAF_E_64 8
+#endif
+#ifndef GRAF_S_64
+#define GRAF_S_64 16
+#endif
+#ifndef GRAF_E_128
+#define GRAF_E_128 16
+#endif
+#ifndef GRAF_S_128
+#define GRAF_S_128 16
+#endif
+#ifndef GRAF_E_256
+#define GRAF_E_256 16
+#endif
+#ifndef GRAF_S_256
+#define GRAF_S_256 8
+#endif
+#ifndef GRAF_E_512
+#define GRAF_E_512 8
+#endif
+#ifndef GRAF_S_512
+#define GRAF_S_512 2
+#endif
+#ifndef GRAF_E_1024
+#define GRAF_E_1024 16
+#endif
+#ifndef GRAF_S_1024
+#define GRAF_S_1024 2
+#endif
+#ifndef GRAF_E_2048
+#define GRAF_E_2048 16
+#endif
+#ifndef GRAF_S_2048
+#define GRAF_S_2048 1
+#endif
+#ifndef GRAF_E_4096
+#define GRAF_E_4096 16
+#endif
+#ifndef GRAF_S_4096
+#define GRAF_S_4096 1
+#endif
+#ifndef GRAF_E_8192
+#define GRAF_E_8192 16
+#endif
+#ifndef GRAF_S_8192
+#define GRAF_S_8192 1
+#endif
+#ifndef GRAF_E_16384
+#define GRAF_E_16384 16
+#endif
 GRAF_CFG(2, 2, 64)
 GRAF_CFG(4, 4, 64)
 GRAF_CFG(8, 8, 64)
 GRAF_CFG(16, 16, 64)
 GRAF_CFG(32, 16, 32)
-GRAF_CFG(64, 8, 16)
-GRAF_CFG(128, 16, 16)
-GRAF_CFG(256, 16, 8)
-GRAF_CFG(512, 8, 2)
-GRAF_CFG(1024, 16, 2)
-GRAF_CFG(2048, 16, 1)
-GRAF_CFG(4096, 16, 1)
-GRAF_CFG(8192, 16, 1)
-GRAF_CFG(16384, 16, 1)
+GRAF_CFG(64, GRAF_E_64, GRAF_S_64)
+GRAF_CFG(128, GRAF_E_128, GRAF_S_128)
+GRAF_CFG(256, GRAF_E_256, GRAF_S_256)
+GRAF_CFG(512, GRAF_E_512, GRAF_S_512)
+GRAF_CFG(1024, GRAF_E_1024, GRAF_S_1024)
+GRAF_CFG(2048, GRAF_E_2048, GRAF_S_2048)
+GRAF_CFG(4096, GRAF_E_4096, GRAF_S_4096)
+GRAF_CFG(8192, GRAF_E_8192, GRAF_S_8192)
+GRAF_CFG(16384, GRAF_E_16384, 1)
 #undef GRAF_CFG
 
 template <int T, int S>
@@ -266,9 +318,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int n = t + e * T;
-        float2 r = make_float2(0.f, 0.f);
-        if (valid && n >= lo && n < hi) r = cmulc(sv[n], sv[n - k]);
-        v[e] = r;
+        const bool in = valid && n >= lo && n < hi;
+        const int n1 = in ? n : 0, n2 = in ? n - k : 0;   // clamped: loads stay in bounds, no branch
+        const float2 r = cmulc(sv[n1], sv[n2]);
+        v[e] = in ? r : make_float2(0.f, 0.f);
       }
       // ---- a2: forward Doppler FFT
       fft_rows<M, E, 0, false>(v, sh, t, tw, sync);
@@ -393,11 +446,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
       if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
       if (do_adj) {
         fft_rows<M, E, 0, true>(v, sh, t, tw, sync);
+        // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n]
+        // (indices clamped so every load is in bounds; the update is predicated, not branched)
         if (lrow) {
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int n = t + e * T;
-            if (n >= lo && n < hi) gacc[n] = cadd(gacc[n], cmul(v[e], sv[n - k]));  // term 1 at p = n
+            const bool in = n >= lo && n < hi;
+            const int n1 = in ? n : 0, n2 = in ? n - k : 0;
+            const float2 a = cadd(gacc[n1], cmul(v[e], sv[n2]));
+            if (in) gacc[n1] = a;
           }
         }
         sync();
@@ -405,7 +463,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int n = t + e * T;
-            if (n >= lo && n < hi) gacc[n - k] = cadd(gacc[n - k], cmulc(sv[n], v[e]));  // term 2 at p = n-k
+            const bool in = n >= lo && n < hi;
+            const int n1 = in ? n : 0, n2 = in ? n - k : 0;
+            const float2 a = cadd(gacc[n2], cmulc(sv[n1], v[e]));
+            if (in) gacc[n2] = a;
           }
         }
         sync();
