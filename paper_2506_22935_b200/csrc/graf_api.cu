@@ -73,7 +73,7 @@ struct Plan {
   bool fixedP = false;
   bool s_smem = true, g_smem = true;
   size_t smem = 0;
-  size_t off_part = 0, off_gpart = 0, off_comb = 0, total = 0;
+  size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
 };
 
 struct CfgInfo {
@@ -209,7 +209,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
       pl.U = 0;
     }
   }
-  pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
+  pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? (size_t)ci.S * N : 0));
   // Upper bound on CTAs per waveform (sizes the workspace); the launch picks the
   // actual P <= bound from the kernel's measured occupancy (choose_P).
@@ -225,6 +225,8 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   if (grad) off = align256(off + sizeof(float2) * (size_t)B * pl.Pbound * N);
   pl.off_comb = off;
   off = align256(off + sizeof(graf_partials) * (size_t)B);
+  pl.off_spad = off;
+  if (!ci.s_smem) off = align256(off + sizeof(float2) * (size_t)B * (N + af->m));
   pl.total = off;
   return pl;
 }
@@ -268,11 +270,12 @@ cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
 
 template <int M, int KIND, bool WGT>
 cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
+  int occ = 1, nsm = kNumSM;
+  // (also sets the instantiation's large-shared-memory attribute, once per device)
+  cudaError_t e0 = kernel_occupancy<M, KIND, WGT>(pl.smem, &occ, &nsm);
+  if (e0 != cudaSuccess) return e0;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
   if (!pl.fixedP) {
-    int occ = 1, nsm = kNumSM;
-    cudaError_t e = kernel_occupancy<M, KIND, WGT>(pl.smem, &occ, &nsm);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorInvalidConfiguration;
     pl.P = choose_P(pl, B, occ, nsm);
     pl.fixedP = true;   // later passes of the same call reuse it
   }
@@ -366,7 +369,18 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
   char* w = static_cast<char*>(ws);
   rp.part = reinterpret_cast<double*>(w + pl.off_part);
   rp.gpart = reinterpret_cast<float2*>(w + pl.off_gpart);
+  rp.s_pad = pl.s_smem ? nullptr : reinterpret_cast<const float2*>(w + pl.off_spad);
   return rp;
+}
+
+// global zero-padded s for the sizes whose s does not fit in shared memory
+cudaError_t prepare_spad(const Plan& pl, const graf_af_desc* af, const void* s, void* ws, cudaStream_t st) {
+  if (pl.s_smem) return cudaSuccess;
+  float2* sp = reinterpret_cast<float2*>(static_cast<char*>(ws) + pl.off_spad);
+  const long long total = af->batch * (long long)(af->n + af->m);
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  pad_s_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(s), sp, af->n, af->m, af->batch);
+  return cudaGetLastError();
 }
 
 graf_status common_checks(const graf_af_desc* af, const graf_loss_desc* L, const void* s, void* surface,
@@ -493,6 +507,7 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  if (pl.U > 0 && (e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
   RowParams rp = base_params(af, s, pl, ws);
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
   if (loss) fill_loss(rp, af, loss);
@@ -532,6 +547,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     if (loss_out && !global) return fail(GRAF_EINVAL, "shard with no rows cannot compute the loss without `global`");
     // loss from global partials via the finalize path with P partial records absent
   }
+  if (pl.U > 0 && (e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
   RowParams rp = base_params(af, s, pl, ws);
   fill_loss(rp, af, loss);
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
@@ -585,6 +601,7 @@ graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* 
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  if ((e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
   RowParams rp = base_params(af, s, pl, ws);
   rp.dA = static_cast<const float2*>(dA);
   prof_mark(true, cs);

@@ -19,9 +19,9 @@
 // Twiddles: the per-thread base twiddle W_M^{(j' mod Ns) M/(Ns R)} of every
 // (pass, q) depends only on the thread, so it is read once per kernel from the
 // correctly rounded table g_tw into registers; the R-1 powers are rebuilt per
-// use by a balanced product tree (depth <= log2 R, error <= ~4 ulp).  When the
-// whole plan has a single twiddled butterfly per thread, all powers stay cached
-// in registers.
+// use by a balanced product tree (depth <= log2 R, error <= ~4 ulp).  When a
+// thread needs at most 16 twiddles per FFT (M <= 256 with E = 16), all of them
+// are computed once per kernel and stay cached in registers for every row.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -127,11 +127,13 @@ __device__ __forceinline__ int padded(int y) {
   return y + (y >> ilog2(E));
 }
 
-// ---- compile-time pass plan: radices E, E, ..., remainder
+// ---- compile-time pass plan: radices RM, RM, ..., remainder, with RM = min(E, 16)
+// (a thread with E = 32 values runs two radix-16 butterflies per pass)
+__host__ __device__ constexpr int max_radix(int E) { return E > 16 ? 16 : E; }
 __host__ __device__ constexpr int pass_radix(int M, int E, int p) {
   int ns = 1;
-  for (int i = 0; i < p; ++i) ns *= (M / ns >= E ? E : M / ns);
-  return M / ns >= E ? E : M / ns;
+  for (int i = 0; i < p; ++i) ns *= (M / ns >= max_radix(E) ? max_radix(E) : M / ns);
+  return M / ns >= max_radix(E) ? max_radix(E) : M / ns;
 }
 __host__ __device__ constexpr int pass_ns(int M, int E, int p) {
   int ns = 1;
@@ -159,15 +161,27 @@ __device__ __forceinline__ void tw_powers(float2 w1, float2* w) {
   for (int r = 2; r < R; ++r) w[r] = cmul(w[r / 2], w[r - r / 2]);
 }
 
+// total twiddle multiplies per thread per FFT (passes >= 1)
+__host__ __device__ constexpr int tw_count(int M, int E) {
+  int n = 0;
+  for (int p = 1; p < num_passes(M, E); ++p) n += (E / pass_radix(M, E, p)) * (pass_radix(M, E, p) - 1);
+  return n;
+}
+__host__ __device__ constexpr int tw_count_before(int M, int E, int P) {
+  int n = 0;
+  for (int p = 1; p < P; ++p) n += (E / pass_radix(M, E, p)) * (pass_radix(M, E, p) - 1);
+  return n;
+}
+
 template <int M, int E>
 struct Twiddles {
   static constexpr int T = M / E;
   static constexpr int NP = num_passes(M, E);
   static constexpr int NB = tw_offset(M, E, NP);          // base twiddles per thread
-  static constexpr bool CACHE = (NB == 1);                // single twiddled butterfly: keep all powers
-  static constexpr int RC = CACHE ? pass_radix(M, E, 1) : 1;
-  float2 base[NB > 0 ? NB : 1];
-  float2 pw[RC];
+  static constexpr int NTW = tw_count(M, E);              // all twiddles per thread
+  static constexpr bool CACHE = (NTW > 0 && NTW <= 16);   // keep every power in registers
+  float2 base[NB > 0 && !CACHE ? NB : 1];
+  float2 pw[CACHE ? NTW : 1];
 
   __device__ __forceinline__ void init(int t) {
 #pragma unroll
@@ -176,10 +190,26 @@ struct Twiddles {
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const int jm = (t + q * T) & (ns - 1);
-        base[tw_offset(M, E, p) + q] = g_tw[(jm * (M / (ns * R))) * (kMaxM / M)];
+        const float2 w1 = g_tw[(jm * (M / (ns * R))) * (kMaxM / M)];
+        if constexpr (CACHE) {
+          float2 w[32];
+          tw_powers_rt(w1, w, R);
+#pragma unroll
+          for (int r = 1; r < R; ++r) pw[tw_count_before(M, E, p) + q * (R - 1) + r - 1] = w[r];
+        } else {
+          base[tw_offset(M, E, p) + q] = w1;
+        }
       }
     }
-    if constexpr (CACHE) tw_powers<RC>(base[0], pw);
+  }
+
+  __device__ __forceinline__ static void tw_powers_rt(float2 w1, float2* w, int R) {
+    // R is a compile-time constant after unrolling; dispatch keeps tw_powers templated
+    if (R == 2) tw_powers<2>(w1, w);
+    else if (R == 4) tw_powers<4>(w1, w);
+    else if (R == 8) tw_powers<8>(w1, w);
+    else if (R == 16) tw_powers<16>(w1, w);
+    else if (R == 32) tw_powers<32>(w1, w);
   }
 };
 
@@ -198,8 +228,12 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
     for (int r = 0; r < R; ++r) x[r] = v[q + r * Q];
     if constexpr (NS > 1) {
       if constexpr (Twiddles<M, E>::CACHE) {
+        constexpr int off = tw_count_before(M, E, P);
 #pragma unroll
-        for (int r = 1; r < R; ++r) x[r] = INV ? cmulc(x[r], tw.pw[r]) : cmul(x[r], tw.pw[r]);
+        for (int r = 1; r < R; ++r) {
+          const float2 w = tw.pw[off + q * (R - 1) + r - 1];
+          x[r] = INV ? cmulc(x[r], w) : cmul(x[r], w);
+        }
       } else {
         float2 w[R];
         tw_powers<R>(tw.base[tw_offset(M, E, P) + q], w);

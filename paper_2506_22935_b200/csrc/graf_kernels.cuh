@@ -53,6 +53,7 @@ struct RowParams {
   // outputs
   double* part;        // [B][P][kPart]
   float2* gpart;       // [B][P][N]
+  const float2* s_pad; // [B][N+M] zero-padded s (global-memory path, M > 8192)
 };
 
 template <int M>
@@ -117,7 +118,7 @@ struct Cfg;
 #define GRAF_S_8192 1
 #endif
 #ifndef GRAF_E_16384
-#define GRAF_E_16384 16
+#define GRAF_E_16384 32
 #endif
 GRAF_CFG(2, 2, 64)
 GRAF_CFG(4, 4, 64)
@@ -217,10 +218,28 @@ __device__ __forceinline__ void lse_merge(float& m, double& Z, float m2, double 
 // float exp(x) for x <= 0 through the MUFU ex2 unit (rel. error ~2 ulp)
 __device__ __forceinline__ float exp_fast(float x) { return exp2f(x * 1.4426950408889634f); }
 
+// minimum resident CTAs per SM requested from ptxas (caps registers per thread);
+// a tuning build may force one value for every size with -DGRAF_MINB=..
+template <int M>
+struct MinBlocks {
+#ifdef GRAF_MINB
+  static constexpr int value = GRAF_MINB;
+#else
+  static constexpr int value = M <= 16 ? 2 : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
+#endif
+};
+// bits e of [e_lo, e_hi) as a mask over the E register slots
+__device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi) {
+  const unsigned long long hi = e_hi >= 64 ? ~0ull : ((1ull << e_hi) - 1ull);
+  const unsigned long long lo = e_lo >= 64 ? ~0ull : ((1ull << e_lo) - 1ull);
+  return hi & ~lo;
+}
+
 template <int M, int KIND, bool WGT>
-__global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
+__global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
+  constexpr int LT = ilog2(T);
   constexpr bool GRAD = (KIND != K_FWD);
   extern __shared__ float4 smem_raw[];
   float2* smem = reinterpret_cast<float2*>(smem_raw);
@@ -232,17 +251,21 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float2* sg = p.s + (size_t)b * N;
 
-  // ---- shared-memory carve-up: [scratch 64 doubles][s][exchange x S][g x S]
+  // ---- shared-memory carve-up: [scratch 64 doubles][s_pad N+M][exchange x S][g x S]
+  // s_pad holds s[n] for n in [-N, M): N zeros, the N samples, M-N zeros, so the
+  // lag product and the correlation read s[n-k] with no bounds arithmetic.
   double* red = reinterpret_cast<double*>(smem);
-  float2* s_sh = smem + 64;
-  float2* xch = s_sh + (C::S_SMEM ? ((N + 1) & ~1) : 0);
+  float2* s_pad = smem + 64;
+  const int NP2 = (N + M + 1) & ~1;
+  float2* xch = s_pad + (C::S_SMEM ? NP2 : 0);
   float2* gacc_sh = xch + S * XS;
-  const float2* sv = C::S_SMEM ? s_sh : sg;
+  const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
   float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * N : p.gpart + ((size_t)b * P + pb) * N;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
   if constexpr (C::S_SMEM) {
-    for (int i = threadIdx.x; i < N; i += THREADS) s_sh[i] = sg[i];
+    for (int i = threadIdx.x; i < N + M; i += THREADS)
+      s_pad[i] = (i >= N && i < 2 * N) ? sg[i - N] : make_float2(0.f, 0.f);
   }
   if constexpr (GRAD) {
     if constexpr (C::G_SMEM) {
@@ -298,6 +321,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
   const int rows_per_iter = P * S;
   const int iters = (p.U + rows_per_iter - 1) / rows_per_iter;
   const size_t surf_rows = (size_t)(p.ke - p.kb);
+  const int lay = p.layout ? M / 2 : 0;
 
   for (int it = 0; it < iters; ++it) {
     const int u = it * rows_per_iter + pb * S + slot;
@@ -305,23 +329,24 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
     const int k = p.row_lo + (valid ? u : 0) * p.row_step;
     const int lo = k > 0 ? k : 0;
     const int hi = k < 0 ? N + k : N;
+    // slots e whose time index n = t + e*T lies in the row's support [lo, hi)
+    const unsigned long long vmask =
+        slot_range_mask(lo > t ? (lo - t + T - 1) >> LT : 0, hi > t ? (hi - t + T - 1) >> LT : 0);
     float2 v[E];
     bool lrow;
-    float mult;
 
     if constexpr (KIND != K_ADJ) {
-      // ---- a1: lag product into the first-pass registers (time index n = t + e*T)
+      // ---- a1: lag product into the first-pass registers (time index n = t + e*T);
+      //      s_pad makes out-of-support terms exactly zero
       const bool wpos = valid && p.surface && k >= p.kb && k < p.ke;
       const bool wneg = valid && p.surface && k > 0 && -k >= p.kb && -k < p.ke;
       lrow = valid && p.loss_on && k <= p.kloss && (k % p.shard_count) == p.shard_index;
-      mult = (k == 0) ? 1.f : 2.f;
+      const float mult = (k == 0) ? 1.f : 2.f;
+      {
+        const float2* a = sv + t;
+        const float2* c = sv + t - k;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int n = t + e * T;
-        const bool in = valid && n >= lo && n < hi;
-        const int n1 = in ? n : 0, n2 = in ? n - k : 0;   // clamped: loads stay in bounds, no branch
-        const float2 r = cmulc(sv[n1], sv[n2]);
-        v[e] = in ? r : make_float2(0.f, 0.f);
+        for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
       }
       // ---- a2: forward Doppler FFT
       fft_rows<M, E, 0, false>(v, sh, t, tw, sync);
@@ -329,7 +354,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
       if (wpos || wneg) {
         const float nrm = p.norm_out ? invE : 1.f;
-        const int lay = p.layout ? M / 2 : 0;
+        // column of frequency m in row +k: (m + lay) mod M; in row -k: (lay - m) mod M
         if (p.out_kind == GRAF_OUT_C64) {
           float2* out = reinterpret_cast<float2*>(p.surface);
           float2* rp = out + ((size_t)b * surf_rows + (k - p.kb)) * M;
@@ -337,12 +362,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int m = t + e * T;
-            if (wpos) __stcs(rp + ((m + lay) & (M - 1)), cscale(v[e], nrm));
+            if (wpos) __stcs(rp + t + (e < E / 2 ? e * T + lay : e * T - lay), cscale(v[e], nrm));
             if (wneg) {
-              const int mn = (M - m) & (M - 1);
-              // A[-k, mn] = e^{+2 pi i mn k / M} conj(A[k, m]) = conj(W^{mn k} A)
-              const float2 w = g_tw[(int)(((long long)mn * k) & (M - 1)) * (kMaxM / M)];
-              __stcs(rn + ((mn + lay) & (M - 1)), cscale(cconj(cmul(w, v[e])), nrm));
+              // A[-k, -m] = e^{-2 pi i m k / M} conj(A[k, m]) = conj(W^{-mk} A) with W^{-mk} = conj(g_tw)
+              const float2 w = g_tw[(int)(((long long)m * k) & (M - 1)) * (kMaxM / M)];
+              __stcs(rn + ((lay - m) & (M - 1)), cscale(cconj(cmulc(v[e], w)), nrm));
             }
           }
         } else {
@@ -355,9 +379,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
           for (int e = 0; e < E; ++e) {
             const int m = t + e * T;
             const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-            const float val = (absk ? sqrtf(chi) : chi) * sc;
-            if (wpos) __stcs(rp + ((m + lay) & (M - 1)), val);
-            if (wneg) __stcs(rn + (((M - m) + lay) & (M - 1)), val);
+            const float val = (absk ? (chi > 0.f ? chi * rsqrtf(chi) : 0.f) : chi) * sc;
+            if (wpos) __stcs(rp + t + (e < E / 2 ? e * T + lay : e * T - lay), val);
+            if (wneg) __stcs(rn + ((lay - m) & (M - 1)), val);
           }
         }
       }
@@ -430,14 +454,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
     } else {
       // ---- K_ADJ: G = dA row (unfolded k = kb + u)
       lrow = valid;
-      mult = 1.f;
-      const float2* drow = p.dA + ((size_t)b * surf_rows + (k - p.kb)) * M;
-      const int lay = p.layout ? M / 2 : 0;
+      const float2* drow = p.dA + ((size_t)b * surf_rows + (k - p.kb)) * M + t;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int m = t + e * T;
-        v[e] = valid ? __ldcs(drow + ((m + lay) & (M - 1))) : make_float2(0.f, 0.f);
-      }
+      for (int e = 0; e < E; ++e)
+        v[e] = valid ? __ldcs(drow + (e < E / 2 ? e * T + lay : e * T - lay)) : make_float2(0.f, 0.f);
     }
 
     // ---- a6 + a7: inverse Doppler FFT and the delay correlation
@@ -446,28 +466,23 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
       if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
       if (do_adj) {
         fft_rows<M, E, 0, true>(v, sh, t, tw, sync);
-        // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n]
-        // (indices clamped so every load is in bounds; the update is predicated, not branched)
-        if (lrow) {
+        // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n],
+        // for n in the row's support (vmask); each address is touched once per phase.
+        const unsigned long long m1 = lrow ? vmask : 0ull;
+        {
+          float2* g1 = gacc + t;
+          const float2* s1 = sv + t - k;
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int n = t + e * T;
-            const bool in = n >= lo && n < hi;
-            const int n1 = in ? n : 0, n2 = in ? n - k : 0;
-            const float2 a = cadd(gacc[n1], cmul(v[e], sv[n2]));
-            if (in) gacc[n1] = a;
-          }
+          for (int e = 0; e < E; ++e)
+            if (m1 & (1ull << e)) g1[e * T] = cadd(g1[e * T], cmul(v[e], s1[e * T]));
         }
         sync();
-        if (lrow) {
+        {
+          float2* g2 = gacc + t - k;
+          const float2* s2 = sv + t;
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int n = t + e * T;
-            const bool in = n >= lo && n < hi;
-            const int n1 = in ? n : 0, n2 = in ? n - k : 0;
-            const float2 a = cadd(gacc[n2], cmulc(sv[n1], v[e]));
-            if (in) gacc[n2] = a;
-          }
+          for (int e = 0; e < E; ++e)
+            if (m1 & (1ull << e)) g2[e * T] = cadd(g2[e * T], cmulc(s2[e * T], v[e]));
         }
         sync();
       }
@@ -517,6 +532,18 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS) af_rows_kernel(RowParams p) {
       for (int sl = 1; sl < S; ++sl) a = cadd(a, gacc_sh[(size_t)sl * N + n]);
       gout[n] = a;
     }
+  }
+}
+
+// zero-padded copy of s for the global-memory path: s_pad[b][i] = s[b][i - N] for
+// i in [N, 2N), 0 elsewhere in [0, N + M)
+__global__ void pad_s_kernel(const float2* s, float2* s_pad, int N, int M, long long B) {
+  const long long total = B * (long long)(N + M);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / (N + M);
+    const int j = (int)(i - b * (N + M));
+    s_pad[i] = (j >= N && j < 2 * N) ? s[b * N + (j - N)] : make_float2(0.f, 0.f);
   }
 }
 
