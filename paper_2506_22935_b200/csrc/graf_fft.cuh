@@ -122,18 +122,34 @@ __device__ __forceinline__ void dft(float2* x) {
 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
+// exchange-buffer padding: one pad slot every max-radix elements (conflict-free
+// for every plan used; scripts/bank_sim.py)
 template <int E>
 __device__ __forceinline__ int padded(int y) {
-  return y + (y >> ilog2(E));
+  return y + (y >> ilog2(E > 16 ? 16 : E));
 }
 
-// ---- compile-time pass plan: radices RM, RM, ..., remainder, with RM = min(E, 16)
-// (a thread with E = 32 values runs two radix-16 butterflies per pass)
+// ---- compile-time pass plan: radices RM, RM, ..., remainder (GRAF_REM_FIRST=1
+// puts the remainder first), with RM = min(E, 16) (a thread with E = 32 values
+// runs two radix-16 butterflies per pass)
 __host__ __device__ constexpr int max_radix(int E) { return E > 16 ? 16 : E; }
+__host__ __device__ constexpr int first_radix(int M, int E) {
+  int m = M;
+  while (m >= max_radix(E)) m /= max_radix(E);
+  return m > 1 ? m : max_radix(E) <= M ? max_radix(E) : M;
+}
+#ifndef GRAF_REM_FIRST
+#define GRAF_REM_FIRST 0
+#endif
 __host__ __device__ constexpr int pass_radix(int M, int E, int p) {
+#if GRAF_REM_FIRST
+  return p == 0 ? first_radix(M, E) : max_radix(E);
+#else
+  // remainder LAST: RM, RM, ..., M / RM^k
   int ns = 1;
   for (int i = 0; i < p; ++i) ns *= (M / ns >= max_radix(E) ? max_radix(E) : M / ns);
   return M / ns >= max_radix(E) ? max_radix(E) : M / ns;
+#endif
 }
 __host__ __device__ constexpr int pass_ns(int M, int E, int p) {
   int ns = 1;

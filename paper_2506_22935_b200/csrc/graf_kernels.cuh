@@ -20,6 +20,7 @@
 // rows +k and -k (loss sums and gradient terms counted twice; SURVEY §8(c)
 // "symmetric-loss identities").
 #pragma once
+#include <type_traits>
 #include "../../include/graf.h"
 #include "graf_fft.cuh"
 
@@ -64,7 +65,7 @@ struct Cfg;
   struct Cfg<M_> {                                                   \
     static constexpr int M = M_, E = E_, T = M_ / E_, S = S_;        \
     static constexpr int THREADS = T * S;                            \
-    static constexpr int XS = M_ + M_ / E_; /* padded exchange */    \
+    static constexpr int XS = M_ + M_ / (E_ > 16 ? 16 : E_); /* padded exchange */ \
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
     static constexpr bool G_SMEM = (M_ <= 8192);                     \
   };
@@ -281,14 +282,15 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   Twiddles<M, E> tw;
   tw.init(t);
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
-  unsigned band = 0u, mlb = 0u;
+  using Mask = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
+  Mask band = 0, mlb = 0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int m = t + e * T;
     const int d = m < M / 2 ? m : m - M;
     const int ad = d < 0 ? -d : d;
-    band |= (ad <= p.d_max ? 1u : 0u) << e;
-    mlb |= (ad <= p.ml_d ? 1u : 0u) << e;
+    band |= (Mask)(ad <= p.d_max ? 1 : 0) << e;
+    mlb |= (Mask)(ad <= p.ml_d ? 1 : 0) << e;
   }
   __syncthreads();
   const double Ed = red[0];
@@ -388,12 +390,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
 
       // ---- a3L (+ a5): loss partials and the cotangent
       if (lrow) {
-        const unsigned inm = band & ~(k <= p.ml_k ? mlb : 0u);
+        const Mask inm = band & ~(k <= p.ml_k ? mlb : (Mask)0);
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
         float rowS = 0.f, rowM = -INFINITY, rowF = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          if (inm & (1u << e)) {
+          if (inm & ((Mask)1 << e)) {
             float w = 1.f;
             if constexpr (WGT) {
               const int m = t + e * T;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
             float rowZ = 0.f, rowC = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-              if (inm & (1u << e)) {
+              if (inm & ((Mask)1 << e)) {
                 const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
                 const float x = p.normalize ? chi * invE2 : chi;
                 rowZ += exp_fast((x - accM) * p.invT);
