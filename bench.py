@@ -245,16 +245,32 @@ def main():
     stream = torch.cuda.Stream(dev)
     ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+    delay = (w["cid"] == 5 and world > 1)   # c5: delay-axis sharding with NCCL exchange (strong scaling)
+    if delay:
+        from paper_2506_22935_b200 import sharding
+        s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=0)).pin_memory()
+        s = s_host.to(dev)
+        tb = TimedBackend(graf, sharding)
+
     def call(st=None):
+        if delay:
+            sharding.delay_sharded_loss_grad(s, M, spec, backend=tb)
+            return
         graf.af_loss_grad(s, M, spec, out=out, layout="centered", ws=ws, grad=grad, loss_out=loss_out,
                           surface=surf, stream=st)
 
     with torch.cuda.stream(stream):
         call(stream)                                    # twiddle init + workspace, before capture
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=stream):
-        call(stream)
+    if delay:
+        class _Eager:                     # NCCL step: eager replay (no graph)
+            def replay(self_inner):
+                call(stream)
+        g = _Eager()
+    else:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            call(stream)
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
@@ -290,17 +306,25 @@ def main():
     # dominant kernel(s): the ABI records ev_k0/ev_k1 around its delay-row kernels
     # (graf_set_profile_events); eager calls, same inputs, same L2 flush protocol.
     L = graf.lib()
-    ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
-    ev_k1.record(stream)
-    torch.cuda.synchronize()
-    L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
-    with torch.cuda.stream(stream):
-        for i in range(args.steps):
-            flush.zero_()
-            call(stream)
-            ev_k1.synchronize()
-            kern_ms.append(ev_k0.elapsed_time(ev_k1))
-    L.graf_set_profile_events(None, None)
+    if delay:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.zero_()
+                call(stream)
+                torch.cuda.synchronize()
+                kern_ms.append(tb.kernel_ms())
+    else:
+        ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
+        ev_k1.record(stream)
+        torch.cuda.synchronize()
+        L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.zero_()
+                call(stream)
+                ev_k1.synchronize()
+                kern_ms.append(ev_k0.elapsed_time(ev_k1))
+        L.graf_set_profile_events(None, None)
     total_ms = sum(step_ms)
     kern_avg = sum(kern_ms) / len(kern_ms)
     if world > 1:
@@ -308,7 +332,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, kern_avg = t.tolist()
     ms_per_step = total_ms / args.steps
-    value = world * B * args.steps / (total_ms / 1e3)
+    units = B if delay else world * B           # delay sharding: the ranks share one batch
+    value = units * args.steps / (total_ms / 1e3)
 
     # ---- e2e: public API, pinned host buffers, H2D + call + D2H inside the timed region
     g_host = torch.empty((B, N), dtype=torch.complex64).pin_memory()
@@ -321,8 +346,11 @@ def main():
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             s_dev2.copy_(s_host, non_blocking=True)
-            lo, gr, _ = graf.af_loss_grad(s_dev2, M, spec, out=out, layout="centered", ws=ws, surface=surf,
-                                          stream=stream)
+            if delay:
+                lo, gr = sharding.delay_sharded_loss_grad(s_dev2, M, spec)
+            else:
+                lo, gr, _ = graf.af_loss_grad(s_dev2, M, spec, out=out, layout="centered", ws=ws, surface=surf,
+                                              stream=stream)
             l_host.copy_(lo, non_blocking=True)
             g_host.copy_(gr, non_blocking=True)
             b_.record(stream)
@@ -334,10 +362,12 @@ def main():
         t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = t.item()
-    e2e_value = world * B * len(e2e_ms) / (e2e_total / 1e3)
+    e2e_value = units * len(e2e_ms) / (e2e_total / 1e3)
 
     # ---- roofline of the dominant kernel (af_rows_kernel), per launch window
     t_k = kern_avg / 1e3
+    if delay:
+        w["flops"] = w["flops"] / world       # this rank's delay rows
     fl_tf = w["flops"] / t_k / 1e12
     hbm = None
     try:
@@ -366,10 +396,13 @@ def main():
     if rank == 0:
         line = {"metric": "AF forward+loss+grad surfaces/sec", "value": value, "unit": "surfaces/s",
                 "n_gpus": world, "steps": args.steps, "warmup": W, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "higher_is_better": True, "scaling": "strong" if delay else "weak", "vs_baseline": None,
+                "dtype": "f32",
                 "data": "synthetic",
                 "config": {"workload": describe(w), "B_per_gpu": B, "N": N, "M": M,
-                           "cells_per_s": value * N * M, "parallelism": f"batch-sharded x{world} (weak)",
+                           "cells_per_s": value * N * M,
+                           "parallelism": (f"delay-sharded x{world} (NCCL all_gather + all_reduce)" if delay
+                                           else f"batch-sharded x{world} (weak)"),
                            "l2": "flushed between steps (256 MiB memset, outside the events)",
                            "timing": "CUDA-graph replay of graf_af_loss_grad per step, CUDA events",
                            "note": w["note"]},
@@ -377,11 +410,43 @@ def main():
                 "e2e": {"value": e2e_value, "unit": "surfaces/s", "h2d_bytes_per_step": B * N * 8,
                         "d2h_bytes_per_step": B * N * 8 + B * 8,
                         "path": "pinned host s -> H2D -> graf.af_loss_grad (C ABI) -> D2H loss + grad"},
-                "gpu_launches": w["launches"] * args.steps,
+                "gpu_launches": (w["launches"] + (1 if delay else 0)) * args.steps,
                 "clocks": clocks}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+class TimedBackend:
+    """sharding backend that brackets each ABI call's delay-row kernels with events."""
+
+    def __init__(self, graf, sharding):
+        import torch
+        self.inner = sharding.GrafBackend()
+        self.L = graf.lib()
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        for e in self.ev:
+            e.record()
+        torch.cuda.synchronize()
+
+    def _timed(self, i, fn, *a):
+        self.L.graf_set_profile_events(ctypes_ptr(self.ev[2 * i]), ctypes_ptr(self.ev[2 * i + 1]))
+        try:
+            return fn(*a)
+        finally:
+            self.L.graf_set_profile_events(None, None)
+
+    def forward_partials(self, *a):
+        return self._timed(0, self.inner.forward_partials, *a)
+
+    def loss_grad(self, *a):
+        return self._timed(1, self.inner.loss_grad, *a)
+
+    def combine(self, *a):
+        return self.inner.combine(*a)
+
+    def kernel_ms(self):
+        return self.ev[0].elapsed_time(self.ev[1]) + self.ev[2].elapsed_time(self.ev[3])
 
 
 def ctypes_ptr(ev):

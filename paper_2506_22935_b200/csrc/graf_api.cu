@@ -624,34 +624,33 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
   if (G < 1 || B < 1) return fail(GRAF_EINVAL, "G = %d, B = %lld", G, (long long)B);
   const float T = loss->lambda_psl != 0.f ? loss->temperature : 1.f;
   if (!(T > 0.f)) return fail(GRAF_EINVAL, "temperature must be > 0");
-  const float invT = 1.f / T;
   if (on_device) {
-    CombineParams c{shards, G, (int)B, invT, out};
+    CombineParams c{shards, G, (int)B, T, out};
     combine_partials_kernel<<<(unsigned)((B + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(c);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "combine_partials_kernel launch");
   }
   for (int64_t b = 0; b < B; ++b) {
     double S = 0, Z = 0, Cs = 0;
-    float m = -INFINITY;
+    double m = -INFINITY;
     for (int q = 0; q < G; ++q) {
       const graf_partials& g = shards[(size_t)q * B + b];
       S += g.isl_sum;
       Cs += g.cen_sum;
-      const float m2 = (float)g.lse_max;
+      const double m2 = g.lse_max;
       const double Z2 = g.lse_sum;
       if (m2 == -INFINITY) continue;
       if (m == -INFINITY) {
         m = m2;
         Z = Z2;
       } else if (m2 > m) {
-        Z = Z * std::exp((double)(m - m2) * invT) + Z2;
+        Z = Z * std::exp((m - m2) / (double)T) + Z2;
         m = m2;
       } else {
-        Z = Z + Z2 * std::exp((double)(m2 - m) * invT);
+        Z = Z + Z2 * std::exp((m2 - m) / (double)T);
       }
     }
-    out[b] = graf_partials{S, (double)m, Z, Cs};
+    out[b] = graf_partials{S, m, Z, Cs};
   }
   return GRAF_OK;
 }

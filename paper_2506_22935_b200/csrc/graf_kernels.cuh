@@ -201,7 +201,8 @@ __device__ __forceinline__ float block_max_all(float v, double* scratch) {
   }
 }
 
-__device__ __forceinline__ void lse_merge(float& m, double& Z, float m2, double Z2, float invT) {
+// exact merge of (max, sum exp((x - max)/T)) pairs, in double (maxima are exact floats)
+__device__ __forceinline__ void lse_merge(double& m, double& Z, double m2, double Z2, float T) {
   if (m2 == -INFINITY) return;
   if (m == -INFINITY) {
     m = m2;
@@ -209,10 +210,10 @@ __device__ __forceinline__ void lse_merge(float& m, double& Z, float m2, double 
     return;
   }
   if (m2 > m) {
-    Z = Z * exp((double)(m - m2) * invT) + Z2;
+    Z = Z * exp((m - m2) / (double)T) + Z2;
     m = m2;
   } else {
-    Z = Z + Z2 * exp((double)(m2 - m) * invT);
+    Z = Z + Z2 * exp((m2 - m) / (double)T);
   }
 }
 
@@ -564,16 +565,16 @@ __global__ void partials_reduce_kernel(ReduceParams r) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= r.B) return;
   double S = 0, Z = 0, Cs = 0;
-  float m = -INFINITY;
+  double m = -INFINITY;
   for (int q = 0; q < r.P; ++q) {
     const double* rec = r.part + ((size_t)b * r.P + q) * kPart;
     S += rec[0];
     Cs += rec[3];
-    lse_merge(m, Z, (float)rec[1], rec[2], r.invT);
+    lse_merge(m, Z, rec[1], rec[2], r.T);
   }
   graf_partials g;
   g.isl_sum = S;
-  g.lse_max = (double)m;
+  g.lse_max = m;
   g.lse_sum = Z;
   g.cen_sum = Cs;
   r.out[b] = g;
@@ -605,12 +606,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
     if (threadIdx.x == 0) {
       sh[0] = e;
       double S = 0, Z = 0, F = 0;
-      float m = -INFINITY;
+      double m = -INFINITY;
       for (int q = 0; q < f.P; ++q) {
         const double* rec = f.part + ((size_t)b * f.P + q) * kPart;
         S += rec[0];
         F += rec[4];
-        lse_merge(m, Z, (float)rec[1], rec[2], f.invT);
+        lse_merge(m, Z, rec[1], rec[2], f.T);
       }
       sh[1] = F;
       if (f.loss) {
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
 struct CombineParams {
   const graf_partials* shards;
   int G, B;
-  float invT;
+  float T;
   graf_partials* out;
 };
 
@@ -653,12 +654,12 @@ __global__ void combine_partials_kernel(CombineParams c) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= c.B) return;
   double S = 0, Z = 0, Cs = 0;
-  float m = -INFINITY;
+  double m = -INFINITY;
   for (int q = 0; q < c.G; ++q) {
     const graf_partials g = c.shards[(size_t)q * c.B + b];
     S += g.isl_sum;
     Cs += g.cen_sum;
-    lse_merge(m, Z, (float)g.lse_max, g.lse_sum, c.invT);
+    lse_merge(m, Z, g.lse_max, g.lse_sum, c.T);
   }
   graf_partials o;
   o.isl_sum = S;

@@ -1,0 +1,101 @@
+"""Multi-GPU layers over torch.distributed.
+
+One process per GPU.  Two partitionings of the same hot path:
+
+* Batch sharding (configs c2-c4): rank r owns a contiguous block of waveforms;
+  waveforms are independent, so there is NO collective on the data path.
+
+* Delay sharding (config c5, one waveform larger than a single GPU's share):
+  rank r owns the folded delay rows k >= 0 with k % G == r (interleaved, which
+  balances the (N-k)-long lag/correlation work).  The exchange steps are
+    1. soft-PSL only: all_gather of the per-shard partials (isl_sum, lse_max,
+       lse_sum, cen_sum) [B x 32 B], combined in rank order (graf_combine_partials,
+       deterministic) -> every rank holds the global log-sum-exp;
+    2. all_reduce(SUM) of the per-shard gradient g_r [B, N] (complex64), which
+       already includes the shard's share of the normalisation term (linear in
+       its own partial sums), so the sum is the full dL/ds*.
+  ISL-only losses are linear in the per-row sums, so step 1 is skipped and the
+  per-shard losses are summed with the gradient.
+
+`backend` is the object that runs the per-shard compute; the default calls the
+C ABI (graf_af_forward / graf_af_loss_grad / graf_combine_partials).  Tests on CPU
+(gloo, world_size 2) substitute a float64 oracle-backed backend to check the
+exchange logic without a GPU.
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import graf as _graf
+
+__all__ = ["GrafBackend", "batch_slice", "batch_sharded_loss_grad", "delay_sharded_loss_grad"]
+
+
+class GrafBackend:
+    """Per-shard compute through the C ABI (device tensors)."""
+
+    def forward_partials(self, s, M, spec, shard):
+        return _graf.af_forward(s, M, out=None, loss=spec, shard=shard)[1]
+
+    def loss_grad(self, s, M, spec, global_partials, shard):
+        loss, g, _ = _graf.af_loss_grad(s, M, spec, global_partials=global_partials, shard=shard)
+        return loss, g
+
+    def combine(self, spec, parts):
+        return _graf.combine_partials(spec, parts)
+
+
+def _world(group) -> Tuple[int, int]:
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def batch_slice(B: int, rank: int, world: int) -> slice:
+    """Contiguous block of waveforms owned by `rank` (sizes differ by at most 1)."""
+    base, rem = divmod(B, world)
+    start = rank * base + min(rank, rem)
+    return slice(start, start + base + (1 if rank < rem else 0))
+
+
+def batch_sharded_loss_grad(s_all: torch.Tensor, M: int, spec, group=None, backend=None,
+                            gather_loss: bool = False):
+    """Batch sharding: this rank's waveforms only; no data-path collective.
+    Returns (slice, loss[b], grad[b]) for the local block; with gather_loss the
+    full loss vector is all-gathered for reporting (off the hot path)."""
+    backend = backend or GrafBackend()
+    r, G = _world(group)
+    sl = batch_slice(s_all.shape[0], r, G)
+    loss, g = backend.loss_grad(s_all[sl], M, spec, None, (0, 1))
+    if gather_loss and G > 1:
+        parts = [torch.empty_like(loss) for _ in range(G)]
+        dist.all_gather(parts, loss, group=group)   # equal blocks assumed for reporting
+        loss = torch.cat(parts)
+    return sl, loss, g
+
+
+def delay_sharded_loss_grad(s: torch.Tensor, M: int, spec, group=None, backend=None):
+    """Delay sharding of every waveform in `s` across the ranks of `group`.
+    Returns (loss[B] float64, grad[B, N] complex64 = dL/ds*), identical on all ranks."""
+    backend = backend or GrafBackend()
+    r, G = _world(group)
+    shard = (r, G)
+    if G == 1:
+        return backend.loss_grad(s, M, spec, None, (0, 1))
+    if spec.lambda_psl == 0:
+        # ISL-only: one fused pass per shard; loss and gradient are sums over shards
+        loss, g = backend.loss_grad(s, M, spec, None, shard)
+        dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
+        return loss, g
+    # soft-PSL: pass 1 partials -> all_gather -> combine (rank order) -> pass 2 -> all_reduce
+    part = backend.forward_partials(s, M, spec, shard)
+    gathered = [torch.empty_like(part) for _ in range(G)]
+    dist.all_gather(gathered, part.contiguous(), group=group)
+    glob = backend.combine(spec, torch.stack(gathered))
+    loss, g = backend.loss_grad(s, M, spec, glob, shard)
+    dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
+    return loss, g

@@ -1,0 +1,150 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the sharding layer
+(paper_2506_22935_b200/sharding.py): the exchange steps (all_gather of LSE
+partials, rank-order combine, all_reduce of the gradient) must reproduce the
+unsharded result.  The per-shard compute is a float64 oracle-backed stand-in for
+the C ABI (no GPU here); on the GPU the same algebra is checked through the ABI
+in test_gpu_parity.py::test_forward_partials_and_delay_sharding_algebra.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from graf_inputs import SplitMix64, complex_gaussian
+from oracle import graf_oracle as O
+
+
+class OracleShardBackend:
+    """Per-shard quantities from the oracle: folded delay rows k >= 0 with
+    k % G == r stand for the rows +-k of the full region."""
+
+    def __init__(self, N, M):
+        self.N, self.M = N, M
+
+    def _rows(self, spec, shard):
+        r, G = shard
+        K = min(spec.k_max, self.N - 1)
+        return np.array([k for k in range(-K, K + 1) if abs(k) % G == r])
+
+    def _cells(self, s, spec, shard):
+        rows_all, bins, mask, w = O.region(self.N, self.M, spec)
+        keep = np.isin(rows_all, self._rows(spec, shard))
+        A = O.ambiguity(s, self.M, rows_all[keep], bins)
+        return rows_all[keep], bins, mask[keep], w[keep], A
+
+    def forward_partials(self, s_b, M, spec, shard):
+        out = []
+        for s in s_b.numpy():
+            rows, bins, mask, w, A = self._cells(s, spec, shard)
+            E = O.energy(s)
+            chi = np.abs(A) ** 2
+            x = chi / E ** 2 if spec.normalize else chi
+            S = float(np.sum(w[mask] * chi[mask]))
+            if mask.any():
+                c = float(np.max(x[mask]))
+                Z = float(np.sum(np.exp((x[mask] - c) / spec.temperature)))
+            else:
+                c, Z = -np.inf, 0.0
+            out.append([S, c, Z, 0.0])
+        return torch.tensor(out, dtype=torch.float64)
+
+    def combine(self, spec, parts):
+        from paper_2506_22935_b200 import graf
+        return graf.combine_partials(spec, parts)
+
+    def loss_grad(self, s_b, M, spec, glob, shard):
+        if glob is None and spec.lambda_psl != 0:
+            # like graf_af_loss_grad with global = NULL: this call's own partials
+            glob = self.forward_partials(s_b, M, spec, shard)
+        losses, grads = [], []
+        T = spec.temperature
+        for b, s in enumerate(s_b.numpy()):
+            rows, bins, mask, w, A = self._cells(s, spec, shard)
+            E = O.energy(s)
+            chi = np.abs(A) ** 2
+            x = chi / E ** 2 if spec.normalize else chi
+            if glob is not None:
+                S, c, Z = glob[b, 0].item(), glob[b, 1].item(), glob[b, 2].item()
+            else:
+                S, c, Z = float(np.sum(w[mask] * chi[mask])), 0.0, 1.0
+            lse = c + T * np.log(Z)
+            isl = S / E ** 2 if spec.normalize else S
+            losses.append(spec.lambda_isl * isl + (spec.lambda_psl * lse if spec.lambda_psl else 0.0))
+            fp = np.where(mask, spec.lambda_isl * w + spec.lambda_psl * np.exp((x - lse) / T), 0.0)
+            G = fp * A / E ** 2 if spec.normalize else fp * A
+            g = O.adjoint(s, self.M, G, rows, bins)
+            if spec.normalize:
+                g = g - (2.0 / E ** 3) * float(np.sum(fp * chi)) * s
+            grads.append(g)
+        return torch.tensor(losses, dtype=torch.float64), torch.tensor(np.stack(grads))
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_22935_b200 import sharding, LossSpec
+        N, M, spec_d = case
+        s = np.stack([complex_gaussian(SplitMix64(900 + b), N) for b in range(3)]).astype(np.complex128)
+        spec = LossSpec.from_dict(spec_d)
+        be = OracleShardBackend(N, M)
+        loss, g = sharding.delay_sharded_loss_grad(torch.tensor(s), M, spec, backend=be)
+        sl, lb, gb = sharding.batch_sharded_loss_grad(torch.tensor(s), M, spec, backend=be)
+        q.put((rank, loss.numpy(), g.numpy(), (sl.start, sl.stop), lb.numpy(), gb.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [
+    (12, 16, dict(k_max=6, d_max=5, ml_k=0, ml_d=0, lambda_isl=1.0, lambda_psl=0.0, normalize=1)),
+    (12, 16, dict(k_max=11, d_max=8, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05, normalize=1)),
+    (9, 16, dict(k_max=4, d_max=6, ml_k=1, ml_d=0, lambda_isl=0.0, lambda_psl=1.0, temperature=50.0, normalize=0)),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_delay_and_batch_sharding_gloo_world2(case):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N, M, spec_d = case
+    s = np.stack([complex_gaussian(SplitMix64(900 + b), N) for b in range(3)]).astype(np.complex128)
+    ospec = O.LossSpec.from_dict(spec_d)
+    refs = [O.loss_and_grad(s[b], M, ospec) for b in range(3)]
+    L_ref = np.array([r[0] for r in refs])
+    g_ref = np.stack([r[1] for r in refs])
+    for rank, loss, g, (a, z), lb, gb in res:
+        np.testing.assert_allclose(loss, L_ref, rtol=1e-10)
+        np.testing.assert_allclose(g, g_ref, atol=1e-10 * np.abs(g_ref).max())
+        np.testing.assert_allclose(lb, L_ref[a:z], rtol=1e-10)
+        np.testing.assert_allclose(gb, g_ref[a:z], atol=1e-10 * np.abs(g_ref).max())
+    blocks = sorted((a, z) for _, _, _, (a, z), _, _ in res)
+    assert blocks == [(0, 2), (2, 3)]
+
+
+def test_batch_slice_partition():
+    from paper_2506_22935_b200.sharding import batch_slice
+    for B in (1, 7, 256):
+        for G in (1, 2, 3, 8):
+            sl = [batch_slice(B, r, G) for r in range(G)]
+            assert sl[0].start == 0 and sl[-1].stop == B
+            assert all(sl[i].stop == sl[i + 1].start for i in range(G - 1))
+            assert max(x.stop - x.start for x in sl) - min(x.stop - x.start for x in sl) <= 1
