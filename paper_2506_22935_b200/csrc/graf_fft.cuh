@@ -125,8 +125,28 @@ __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x
 // exchange-buffer padding: one pad slot every max-radix elements (conflict-free
 // for every plan used; scripts/bank_sim.py)
 template <int E>
+struct Pad {
+  static constexpr int P = E > 16 ? 16 : E;     // pad period
+  static constexpr int S = ilog2(P);
+};
+template <int E>
 __device__ __forceinline__ int padded(int y) {
-  return y + (y >> ilog2(E > 16 ? 16 : E));
+  return y + (y >> Pad<E>::S);
+}
+// padded(y0 + i*step) for i = 0.. as base + i*stride when step is a multiple of
+// the pad period (affine: one base address + immediate offsets, nothing per element)
+template <int E, int STEP>
+struct PadStride {
+  static constexpr bool AFFINE = (STEP % Pad<E>::P) == 0;
+  static constexpr int value = STEP + STEP / Pad<E>::P;
+};
+
+// opaque copy: stops the compiler from hoisting per-element address math out of
+// the row loop (it would keep ~E addresses live across the whole kernel and spill)
+__device__ __forceinline__ int launder(int x) {
+  int y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
 }
 
 // ---- compile-time pass plan: radices RM, RM, ..., remainder (GRAF_REM_FIRST=1
@@ -196,7 +216,9 @@ struct Twiddles {
   static constexpr int NB = tw_offset(M, E, NP);          // base twiddles per thread
   static constexpr int NTW = tw_count(M, E);              // all twiddles per thread
   static constexpr bool CACHE = (NTW > 0 && NTW <= 16);   // keep every power in registers
+#ifdef GRAF_HOLD_BASES
   float2 base[NB > 0 && !CACHE ? NB : 1];
+#endif
   float2 pw[CACHE ? NTW : 1];
 
   __device__ __forceinline__ void init(int t) {
@@ -213,7 +235,9 @@ struct Twiddles {
 #pragma unroll
           for (int r = 1; r < R; ++r) pw[tw_count_before(M, E, p) + q * (R - 1) + r - 1] = w[r];
         } else {
+#ifdef GRAF_HOLD_BASES
           base[tw_offset(M, E, p) + q] = w1;
+#endif
         }
       }
     }
@@ -252,7 +276,13 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
         }
       } else {
         float2 w[R];
+#ifdef GRAF_HOLD_BASES
         tw_powers<R>(tw.base[tw_offset(M, E, P) + q], w);
+#else
+        // base twiddle re-read per use from the L1-resident table (frees registers)
+        const int jm = (t + q * T) & (NS - 1);
+        tw_powers<R>(__ldg(&g_tw[(jm * (M / (NS * R))) * (kMaxM / M)]), w);
+#endif
 #pragma unroll
         for (int r = 1; r < R; ++r) x[r] = INV ? cmulc(x[r], w[r]) : cmul(x[r], w[r]);
       }
@@ -265,8 +295,18 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
       const int jp = t + q * T;
       const int jm = jp & (NS - 1);
       const int base = (jp / NS) * NS * R + jm;
+      if constexpr (NS == 1 && R <= Pad<E>::P) {
+        float2* b = sh + padded<E>(base);           // base is a multiple of R: no carry
 #pragma unroll
-      for (int r = 0; r < R; ++r) sh[padded<E>(base + r * NS)] = x[r];
+        for (int r = 0; r < R; ++r) b[r] = x[r];
+      } else if constexpr (PadStride<E, NS>::AFFINE) {
+        float2* b = sh + padded<E>(base);
+#pragma unroll
+        for (int r = 0; r < R; ++r) b[r * PadStride<E, NS>::value] = x[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) sh[padded<E>(base + r * NS)] = x[r];
+      }
     }
   }
 }
@@ -281,8 +321,14 @@ __device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, cons
   stockham_pass<M, E, P, INV>(v, sh, t, tw);
   if constexpr (P + 1 < NP) {
     sync();
+    if constexpr (PadStride<E, T>::AFFINE) {
+      const float2* b = sh + padded<E>(t);
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
+      for (int e = 0; e < E; ++e) v[e] = b[e * PadStride<E, T>::value];
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
+    }
     sync();
     fft_rows<M, E, P + 1, INV, Sync>(v, sh, t, tw, sync);
   }

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   const int N = p.N;
   const int b = p.b0 + blockIdx.y;
   const int P = gridDim.x, pb = blockIdx.x;
-  const int slot = threadIdx.x / T, t = threadIdx.x % T;
+  const int slot = threadIdx.x / T, t0 = threadIdx.x % T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float2* sg = p.s + (size_t)b * N;
 
@@ -281,13 +281,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
     if (lane == 0) red[0] = e;
   }
   Twiddles<M, E> tw;
-  tw.init(t);
+  tw.init(t0);
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
   using Mask = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
   Mask band = 0, mlb = 0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int m = t + e * T;
+    const int m = t0 + e * T;
     const int d = m < M / 2 ? m : m - M;
     const int ad = d < 0 ? -d : d;
     band |= (Mask)(ad <= p.d_max ? 1 : 0) << e;
@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   const int lay = p.layout ? M / 2 : 0;
 
   for (int it = 0; it < iters; ++it) {
+    const int t = launder(t0);   // per-row opaque copy of the thread index (see launder())
     const int u = it * rows_per_iter + pb * S + slot;
     const bool valid = u < p.U;
     const int k = p.row_lo + (valid ? u : 0) * p.row_step;
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
       }
       // ---- a2: forward Doppler FFT
       fft_rows<M, E, 0, false>(v, sh, t, tw, sync);
+      asm volatile("" ::: "memory");
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
       if (wpos || wneg) {
@@ -469,6 +471,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
       if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
       if (do_adj) {
         fft_rows<M, E, 0, true>(v, sh, t, tw, sync);
+        // keep the correlation's loads below the last inverse pass (otherwise ptxas
+        // hoists them and holds 2E extra values live across the FFT -> spills)
+        asm volatile("" ::: "memory");
         // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n],
         // for n in the row's support (vmask); each address is touched once per phase.
         const unsigned long long m1 = lrow ? vmask : 0ull;
