@@ -137,6 +137,10 @@ GRAF_CFG(8192, GRAF_E_8192, GRAF_S_8192)
 GRAF_CFG(16384, GRAF_E_16384, 1)
 #undef GRAF_CFG
 
+#ifndef GRAF_GCH
+#define GRAF_GCH 2
+#endif
+
 template <int T, int S>
 struct SlotSync {
   int id;
@@ -219,6 +223,14 @@ __device__ __forceinline__ void lse_merge(double& m, double& Z, double m2, doubl
 
 // float exp(x) for x <= 0 through the MUFU ex2 unit (rel. error ~2 ulp)
 __device__ __forceinline__ float exp_fast(float x) { return exp2f(x * 1.4426950408889634f); }
+
+// expm1(u) to ~1 ulp-scale relative error: degree-7 Taylor on |u| < 0.5 (remainder
+// < u^8/40320 ~ 1e-7 |u|), exp(u) - 1 beyond (no cancellation there)
+__device__ __forceinline__ float expm1_fast(float u) {
+  const float p = fmaf(u, fmaf(u, fmaf(u, fmaf(u, fmaf(u, fmaf(u, 1.f / 5040.f, 1.f / 720.f), 1.f / 120.f),
+                                                       1.f / 24.f), 1.f / 6.f), 0.5f), 1.f);
+  return fabsf(u) < 0.5f ? u * p : exp_fast(u) - 1.f;
+}
 
 // minimum resident CTAs per SM requested from ptxas (caps registers per thread);
 // a tuning build may force one value for every size with -DGRAF_MINB=..
@@ -416,7 +428,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
               } else {
                 const float x = p.normalize ? chi * invE2 : chi;
                 if (use_centred) {
-                  fp = p.lam_psl * (expm1f((x - p.xbar) * p.invT) - ebar) * invZc;
+                  fp = p.lam_psl * (expm1_fast((x - p.xbar) * p.invT) - ebar) * invZc;
                 } else {
                   fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);
                 }
@@ -443,7 +455,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
                 const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
                 const float x = p.normalize ? chi * invE2 : chi;
                 rowZ += exp_fast((x - accM) * p.invT);
-                if (p.centred) rowC += expm1f((x - p.xbar) * p.invT);
+                if (p.centred) rowC += expm1_fast((x - p.xbar) * p.invT);
               }
             }
             accZ += (double)(mult * rowZ);
@@ -477,20 +489,52 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
         // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n],
         // for n in the row's support (vmask); each address is touched once per phase.
         const unsigned long long m1 = lrow ? vmask : 0ull;
+        // global-memory accumulator (M = 16384): the loads of each group of CH slots
+        // are issued before its stores, so the RMW pays one L2 latency per group;
+        // shared-memory accumulators use CH = 1 (plain RMW, fewer live registers)
+        constexpr int CH = C::G_SMEM ? 1 : (E < GRAF_GCH ? E : GRAF_GCH);
         {
           float2* g1 = gacc + t;
           const float2* s1 = sv + t - k;
 #pragma unroll
-          for (int e = 0; e < E; ++e)
-            if (m1 & (1ull << e)) g1[e * T] = cadd(g1[e * T], cmul(v[e], s1[e * T]));
+          for (int e0 = 0; e0 < E; e0 += CH) {
+            float2 gv[CH], sv1[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              const int e = e0 + j;
+              if (m1 & (1ull << e)) {
+                gv[j] = g1[e * T];
+                sv1[j] = s1[e * T];
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              const int e = e0 + j;
+              if (m1 & (1ull << e)) g1[e * T] = cadd(gv[j], cmul(v[e], sv1[j]));
+            }
+          }
         }
         sync();
         {
           float2* g2 = gacc + t - k;
           const float2* s2 = sv + t;
 #pragma unroll
-          for (int e = 0; e < E; ++e)
-            if (m1 & (1ull << e)) g2[e * T] = cadd(g2[e * T], cmulc(s2[e * T], v[e]));
+          for (int e0 = 0; e0 < E; e0 += CH) {
+            float2 gv[CH], sv2[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              const int e = e0 + j;
+              if (m1 & (1ull << e)) {
+                gv[j] = g2[e * T];
+                sv2[j] = s2[e * T];
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+              const int e = e0 + j;
+              if (m1 & (1ull << e)) g2[e * T] = cadd(gv[j], cmulc(sv2[j], v[e]));
+            }
+          }
         }
         sync();
       }
