@@ -210,8 +210,18 @@ def main():
     ap.add_argument("--impl", default="graf", choices=["graf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0)
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward"],
+                    help="forward: full-surface mode (graf_af_forward writes the config's surface, no loss)")
     args = ap.parse_args()
     w = workload(args.config)
+    if args.mode == "forward":
+        if not w["cfg"]["surface"]:
+            raise SystemExit("--mode forward needs a config with a surface (c1, c3)")
+        # folded rows covering the whole surface window, one forward FFT each
+        w["flops"] = w["B"] * w["N"] * 5.0 * w["M"] * math.log2(w["M"])
+        w["io_bytes"] = w["B"] * w["N"] * 8
+        w["launches"] = 1
+        w["note"] = "full-surface mode: graf_af_forward writes the surface; no loss or gradient"
     if args.impl == "reference":
         return run_reference(args, w)
 
@@ -255,6 +265,9 @@ def main():
     def call(st=None):
         if delay:
             sharding.delay_sharded_loss_grad(s, M, spec, backend=tb)
+            return
+        if args.mode == "forward":
+            graf.af_forward(s, M, out=out, layout="centered", ws=ws, surface=surf, stream=st)
             return
         graf.af_loss_grad(s, M, spec, out=out, layout="centered", ws=ws, grad=grad, loss_out=loss_out,
                           surface=surf, stream=st)
@@ -339,6 +352,7 @@ def main():
     g_host = torch.empty((B, N), dtype=torch.complex64).pin_memory()
     l_host = torch.empty((B,), dtype=torch.float64).pin_memory()
     s_dev2 = torch.empty_like(s)
+    zrow_host = None
     e2e_ms = []
     with torch.cuda.stream(stream):
         for i in range(W + args.steps):
@@ -348,6 +362,17 @@ def main():
             s_dev2.copy_(s_host, non_blocking=True)
             if delay:
                 lo, gr = sharding.delay_sharded_loss_grad(s_dev2, M, spec)
+            elif args.mode == "forward":
+                sf, _ = graf.af_forward(s_dev2, M, out=out, layout="centered", ws=ws, surface=surf, stream=stream)
+                zrow = sf[:, N - 1, :]                    # zero-delay cut of every surface
+                if zrow_host is None:
+                    zrow_host = torch.empty(zrow.shape, dtype=zrow.dtype).pin_memory()
+                zrow_host.copy_(zrow, non_blocking=True)
+                b_.record(stream)
+                b_.synchronize()
+                if i >= W:
+                    e2e_ms.append(a.elapsed_time(b_))
+                continue
             else:
                 lo, gr, _ = graf.af_loss_grad(s_dev2, M, spec, out=out, layout="centered", ws=ws, surface=surf,
                                               stream=stream)
@@ -394,7 +419,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w)
     if rank == 0:
-        line = {"metric": "AF forward+loss+grad surfaces/sec", "value": value, "unit": "surfaces/s",
+        line = {"metric": ("AF forward+loss+grad surfaces/sec" if args.mode != "forward"
+                           else "AF forward (full-surface) surfaces/sec"), "value": value, "unit": "surfaces/s",
                 "n_gpus": world, "steps": args.steps, "warmup": W, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "strong" if delay else "weak", "vs_baseline": None,
                 "dtype": "f32",
@@ -408,8 +434,11 @@ def main():
                            "note": w["note"]},
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "surfaces/s", "h2d_bytes_per_step": B * N * 8,
-                        "d2h_bytes_per_step": B * N * 8 + B * 8,
-                        "path": "pinned host s -> H2D -> graf.af_loss_grad (C ABI) -> D2H loss + grad"},
+                        "d2h_bytes_per_step": (B * N * 8 + B * 8) if args.mode != "forward" else
+                        B * M * (8 if out == "c64" else 4),
+                        "path": ("pinned host s -> H2D -> graf.af_loss_grad (C ABI) -> D2H loss + grad"
+                                 if args.mode != "forward" else
+                                 "pinned host s -> H2D -> graf.af_forward (C ABI) -> D2H zero-delay cut")},
                 "gpu_launches": (w["launches"] + (1 if delay else 0)) * args.steps,
                 "clocks": clocks}
         print(json.dumps(line))
