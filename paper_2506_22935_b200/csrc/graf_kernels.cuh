@@ -60,14 +60,19 @@ struct RowParams {
 template <int M>
 struct Cfg;
 // E = values per thread, T = threads per row slot, S = row slots per CTA.
+// SPLIT (M = 16384): the row FFT runs as a radix-2 split into two M/2-point
+// sub-FFTs that share one M/2 exchange buffer, so the gradient accumulator fits
+// in shared memory next to it (s is then read from a zero-padded global copy).
 #define GRAF_CFG(M_, E_, S_)                                         \
   template <>                                                        \
   struct Cfg<M_> {                                                   \
     static constexpr int M = M_, E = E_, T = M_ / E_, S = S_;        \
     static constexpr int THREADS = T * S;                            \
-    static constexpr int XS = M_ + M_ / (E_ > 16 ? 16 : E_); /* padded exchange */ \
+    static constexpr bool SPLIT = (M_ >= 16384);                     \
+    static constexpr int MX = SPLIT ? M_ / 2 : M_;  /* exchanged FFT length */ \
+    static constexpr int XS = MX + MX / ((SPLIT ? E_ / 2 : E_) > 16 ? 16 : (SPLIT ? E_ / 2 : E_)); \
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
-    static constexpr bool G_SMEM = (M_ <= 8192);                     \
+    static constexpr bool G_SMEM = true;                             \
   };
 // Defaults; a tuning build may override one size with -DGRAF_E_<M>=.. -DGRAF_S_<M>=..
 #ifndef GRAF_E_64
@@ -136,10 +141,6 @@ GRAF_CFG(4096, GRAF_E_4096, GRAF_S_4096)
 GRAF_CFG(8192, GRAF_E_8192, GRAF_S_8192)
 GRAF_CFG(16384, GRAF_E_16384, 1)
 #undef GRAF_CFG
-
-#ifndef GRAF_GCH
-#define GRAF_GCH 2
-#endif
 
 template <int T, int S>
 struct SlotSync {
@@ -242,6 +243,60 @@ struct MinBlocks {
   static constexpr int value = M <= 16 ? 2 : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
 #endif
 };
+// radix-2 split stage between the two M/2-point halves (twiddle W_M^{t + e T} =
+// W_M^t * W_{2*E2}^e, the second factor a compile-time constant)
+template <int E2, int K, bool INV>
+__device__ __forceinline__ void split_combine(float2* v, const float2* a, const float2* c, float2 wt) {
+  if constexpr (K < E2) {
+    const float2 wb = twc<K, 2 * E2, false>(cmul(c[K], wt));
+    v[K] = cadd(a[K], wb);
+    v[K + E2] = csub(a[K], wb);
+    split_combine<E2, K + 1, INV>(v, a, c, wt);
+  }
+}
+template <int E2, int K>
+__device__ __forceinline__ void split_dif(const float2* v, float2* a, float2* c, float2 wt) {
+  if constexpr (K < E2) {
+    a[K] = cadd(v[K], v[K + E2]);
+    c[K] = twc<K, 2 * E2, true>(cmulc(csub(v[K], v[K + E2]), wt));
+    split_dif<E2, K + 1>(v, a, c, wt);
+  }
+}
+
+// Length-M FFT of one row slot: direct Stockham, or (SPLIT) two M/2-point
+// sub-FFTs of the even/odd time samples joined by one radix-2 stage in registers.
+// Slot layout in frequency is e <-> m = t + e*T either way; in time it is
+// n = t + e*T (direct) or n = 2(t + e'T) + parity (SPLIT, e = e' + parity*E/2).
+template <int M, int E, bool SPLIT, bool INV, class TW, class Sync>
+__device__ __forceinline__ void row_fft(float2 (&v)[E], float2* sh, int t, const TW& tw, const Sync& sync,
+                                        float2 wt) {
+  if constexpr (!SPLIT) {
+    fft_rows<M, E, 0, INV>(v, sh, t, tw, sync);
+  } else {
+    constexpr int E2 = E / 2, M2 = M / 2;
+    float2 a[E2], c[E2];
+    if constexpr (!INV) {
+#pragma unroll
+      for (int e = 0; e < E2; ++e) {
+        a[e] = v[e];
+        c[e] = v[e + E2];
+      }
+      fft_rows<M2, E2, 0, false>(a, sh, t, tw, sync);
+      fft_rows<M2, E2, 0, false>(c, sh, t, tw, sync);
+      split_combine<E2, 0, false>(v, a, c, wt);
+    } else {
+      split_dif<E2, 0>(v, a, c, wt);
+      fft_rows<M2, E2, 0, true>(a, sh, t, tw, sync);
+      fft_rows<M2, E2, 0, true>(c, sh, t, tw, sync);
+#pragma unroll
+      for (int e = 0; e < E2; ++e) {
+        v[e] = a[e];
+        v[e + E2] = c[e];
+      }
+    }
+  }
+}
+
 // bits e of [e_lo, e_hi) as a mask over the E register slots
 __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi) {
   const unsigned long long hi = e_hi >= 64 ? ~0ull : ((1ull << e_hi) - 1ull);
@@ -255,6 +310,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
   constexpr int LT = ilog2(T);
   constexpr bool GRAD = (KIND != K_FWD);
+  constexpr bool SPLIT = C::SPLIT;
+  constexpr int E2 = SPLIT ? E / 2 : E;
   extern __shared__ float4 smem_raw[];
   float2* smem = reinterpret_cast<float2*>(smem_raw);
 
@@ -292,8 +349,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
     const double e = warp_energy(sg, N, lane);
     if (lane == 0) red[0] = e;
   }
-  Twiddles<M, E> tw;
+  Twiddles<C::MX, E2> tw;
   tw.init(t0);
+  const float2 wt = SPLIT ? g_tw[t0 * (kMaxM / M)] : make_float2(1.f, 0.f);  // W_M^t (split stage)
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
   using Mask = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
   Mask band = 0, mlb = 0;
@@ -345,9 +403,19 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
     const int k = p.row_lo + (valid ? u : 0) * p.row_step;
     const int lo = k > 0 ? k : 0;
     const int hi = k < 0 ? N + k : N;
-    // slots e whose time index n = t + e*T lies in the row's support [lo, hi)
-    const unsigned long long vmask =
-        slot_range_mask(lo > t ? (lo - t + T - 1) >> LT : 0, hi > t ? (hi - t + T - 1) >> LT : 0);
+    // slots e whose time index n lies in the row's support [lo, hi)
+    unsigned long long vmask;
+    if constexpr (!SPLIT) {
+      vmask = slot_range_mask(lo > t ? (lo - t + T - 1) >> LT : 0, hi > t ? (hi - t + T - 1) >> LT : 0);
+    } else {
+      // n = 2(t + j T) + par: j in [ceil((lo - par - 2t) / 2T), ceil((hi - par - 2t) / 2T))
+      const int t2 = 2 * t;
+      auto rng = [&](int par) {
+        const int a = lo - par - t2, z = hi - par - t2;
+        return slot_range_mask(a > 0 ? (a + 2 * T - 1) >> (LT + 1) : 0, z > 0 ? (z + 2 * T - 1) >> (LT + 1) : 0);
+      };
+      vmask = rng(0) | (rng(1) << E2);
+    }
     float2 v[E];
     bool lrow;
 
@@ -358,14 +426,22 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
       const bool wneg = valid && p.surface && k > 0 && -k >= p.kb && -k < p.ke;
       lrow = valid && p.loss_on && k <= p.kloss && (k % p.shard_count) == p.shard_index;
       const float mult = (k == 0) ? 1.f : 2.f;
-      {
+      if constexpr (!SPLIT) {
         const float2* a = sv + t;
         const float2* c = sv + t - k;
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
+      } else {
+        const float2* a = sv + 2 * t;
+        const float2* c = sv + 2 * t - k;
+#pragma unroll
+        for (int e = 0; e < E2; ++e) {
+          v[e] = cmulc(a[2 * e * T], c[2 * e * T]);
+          v[e + E2] = cmulc(a[2 * e * T + 1], c[2 * e * T + 1]);
+        }
       }
       // ---- a2: forward Doppler FFT
-      fft_rows<M, E, 0, false>(v, sh, t, tw, sync);
+      row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
       asm volatile("" ::: "memory");
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
@@ -482,59 +558,29 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
       bool do_adj = lrow;
       if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
       if (do_adj) {
-        fft_rows<M, E, 0, true>(v, sh, t, tw, sync);
-        // keep the correlation's loads below the last inverse pass (otherwise ptxas
-        // hoists them and holds 2E extra values live across the FFT -> spills)
+        row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
+        // keep the correlation's loads below the last inverse pass
         asm volatile("" ::: "memory");
         // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n],
         // for n in the row's support (vmask); each address is touched once per phase.
         const unsigned long long m1 = lrow ? vmask : 0ull;
-        // global-memory accumulator (M = 16384): the loads of each group of CH slots
-        // are issued before its stores, so the RMW pays one L2 latency per group;
-        // shared-memory accumulators use CH = 1 (plain RMW, fewer live registers)
-        constexpr int CH = C::G_SMEM ? 1 : (E < GRAF_GCH ? E : GRAF_GCH);
+        // time offset of slot e relative to the thread's base index
+        auto toff = [](int e) { return SPLIT ? (e < E2 ? 2 * e * T : 2 * (e - E2) * T + 1) : e * T; };
+        const int tb = SPLIT ? 2 * t : t;
         {
-          float2* g1 = gacc + t;
-          const float2* s1 = sv + t - k;
+          float2* g1 = gacc + tb;
+          const float2* s1 = sv + tb - k;
 #pragma unroll
-          for (int e0 = 0; e0 < E; e0 += CH) {
-            float2 gv[CH], sv1[CH];
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-              const int e = e0 + j;
-              if (m1 & (1ull << e)) {
-                gv[j] = g1[e * T];
-                sv1[j] = s1[e * T];
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-              const int e = e0 + j;
-              if (m1 & (1ull << e)) g1[e * T] = cadd(gv[j], cmul(v[e], sv1[j]));
-            }
-          }
+          for (int e = 0; e < E; ++e)
+            if (m1 & (1ull << e)) g1[toff(e)] = cadd(g1[toff(e)], cmul(v[e], s1[toff(e)]));
         }
         sync();
         {
-          float2* g2 = gacc + t - k;
-          const float2* s2 = sv + t;
+          float2* g2 = gacc + tb - k;
+          const float2* s2 = sv + tb;
 #pragma unroll
-          for (int e0 = 0; e0 < E; e0 += CH) {
-            float2 gv[CH], sv2[CH];
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-              const int e = e0 + j;
-              if (m1 & (1ull << e)) {
-                gv[j] = g2[e * T];
-                sv2[j] = s2[e * T];
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-              const int e = e0 + j;
-              if (m1 & (1ull << e)) g2[e * T] = cadd(gv[j], cmulc(sv2[j], v[e]));
-            }
-          }
+          for (int e = 0; e < E; ++e)
+            if (m1 & (1ull << e)) g2[toff(e)] = cadd(g2[toff(e)], cmulc(s2[toff(e)], v[e]));
         }
         sync();
       }

@@ -320,3 +320,34 @@ def test_autograd_functions():
     (At.abs() ** 3).sum().backward()
     ref = st.grad.numpy()
     assert np.abs(s2.grad.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+# ------------------------------------------------------------------ M = 16384 (split-FFT kernel path)
+@pytest.mark.parametrize("N,spec_i", [(300, 1), (1000, 0), (129, 4)])
+def test_m16384_loss_grad(N, spec_i):
+    M = 16384
+    s = cg(2, N, 160 + N)
+    spec = dict(SPECS[spec_i], k_max=min(SPECS[spec_i]["k_max"], 40), d_max=min(SPECS[spec_i]["d_max"], 300))
+    check_loss_grad(s, M, spec)
+
+
+def test_m16384_full_plane_small_n():
+    # every delay row of a short waveform at M = 16384, soft-PSL + ISL, raw Doppler window
+    N, M = 64, 16384
+    s = cg(1, N, 77)
+    spec = dict(k_max=N - 1, d_max=600, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.01,
+                normalize=1)
+    check_loss_grad(s, M, spec)
+
+
+@pytest.mark.parametrize("layout", ["raw", "centered"])
+def test_m16384_backward(layout):
+    N, M = 64, 16384
+    s = cg(1, N, 5)
+    kb, ke = -10, 11
+    rows = np.arange(kb, ke)
+    dA = cg(1, len(rows) * M, 6).reshape(1, len(rows), M)
+    g = graf.af_backward(dev(s), M, dev(dA), k_begin=kb, k_end=ke, layout=layout).cpu().numpy()
+    G = dA[0] if layout == "raw" else np.roll(dA[0], -(M // 2), axis=1)
+    ref = O.adjoint(s[0], M, G.astype(np.complex128), rows)
+    assert np.abs(g[0] - ref).max() <= 1e-4 * np.abs(ref).max()
