@@ -73,18 +73,25 @@ struct Plan {
   bool fixedP = false;
   bool s_smem = true, g_smem = true;
   size_t smem = 0;
+  // surface staging for bulk async row stores: per-slot floats,
+  // whether the rows qualify, and whether they fit the slot's exchange buffer (alias)
+  int stg_floats = 0;
+  bool bulk_ok = false, alias_ok = false;
+  size_t smem_stg = 0;
+  int bulk_mode = -1;   // decided at the first launch of a call: 0 direct, 1 dedicated, 2 alias
   size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
 };
 
 struct CfgInfo {
-  int M, E, T, S, threads, XS;
+  int M, E, T, S, threads, XS, tab1;
   bool s_smem, g_smem;
 };
 
 template <int M>
 CfgInfo cfg_info() {
   using C = Cfg<M>;
-  return CfgInfo{M, C::E, C::T, C::S, C::THREADS, C::XS, C::S_SMEM, C::G_SMEM};
+  constexpr int E2 = C::SPLIT ? C::E / 2 : C::E;
+  return CfgInfo{M, C::E, C::T, C::S, C::THREADS, C::XS, Twiddles<C::MX, E2>::TAB1, C::S_SMEM, C::G_SMEM};
 }
 
 bool cfg_for(int M, CfgInfo* ci) {
@@ -210,7 +217,17 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
     }
   }
   pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
-                              (grad && ci.g_smem ? (size_t)ci.S * N : 0));
+                              (grad && ci.g_smem ? (size_t)ci.S * N : 0) + (size_t)ci.tab1);
+  if (kind != Kind::Backward && af->out_kind != GRAF_OUT_NONE) {
+    const size_t row_bytes = (size_t)af->m * (af->out_kind == GRAF_OUT_C64 ? 8 : 4);
+    // the copies move whole rows (raw) or half rows (centred) in 16-byte units
+    if ((af->doppler_layout == GRAF_DOPPLER_CENTERED ? row_bytes / 2 : row_bytes) % 16 == 0) {
+      pl.bulk_ok = true;
+      pl.stg_floats = (int)(2 * row_bytes / 4);
+      pl.smem_stg = (size_t)ci.S * 2 * row_bytes + 16;
+      pl.alias_ok = 2 * row_bytes <= sizeof(float2) * (size_t)ci.XS && ci.XS % 2 == 0;
+    }
+  }
   // Upper bound on CTAs per waveform (sizes the workspace); the launch picks the
   // actual P <= bound from the kernel's measured occupancy (choose_P).
   const long long B = af->batch;
@@ -275,6 +292,28 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   cudaError_t e0 = kernel_occupancy<M, KIND, WGT>(pl.smem, &occ, &nsm);
   if (e0 != cudaSuccess) return e0;
   if (occ < 1) return cudaErrorInvalidConfiguration;
+  size_t smem = pl.smem;
+  if (rp.surface && pl.bulk_ok) {
+    if (pl.bulk_mode < 0) {
+      // dedicated staging unless it costs resident CTAs and the exchange buffer can hold the rows
+      int occ_d = 0;
+      const bool fits = pl.smem + pl.smem_stg <= 227 * 1024;
+      if (fits) {
+        e0 = kernel_occupancy<M, KIND, WGT>(pl.smem + pl.smem_stg, &occ_d, &nsm);
+        if (e0 != cudaSuccess) return e0;
+      }
+      pl.bulk_mode = (fits && (occ_d >= occ || !pl.alias_ok) && occ_d >= 1) ? 1 : pl.alias_ok ? 2 : 0;
+    }
+    rp.bulk = pl.bulk_mode;
+    rp.stg_floats = pl.stg_floats;
+    if (rp.bulk == 1) {
+      smem += pl.smem_stg;
+      e0 = kernel_occupancy<M, KIND, WGT>(smem, &occ, &nsm);
+      if (e0 != cudaSuccess) return e0;
+    }
+  } else {
+    rp.bulk = 0;
+  }
   if (!pl.fixedP) {
     pl.P = choose_P(pl, B, occ, nsm);
     pl.fixedP = true;   // later passes of the same call reuse it
@@ -282,7 +321,8 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   for (int b0 = 0; b0 < B; b0 += 65535) {
     rp.b0 = b0;
     dim3 grid(pl.P, std::min(65535, B - b0));
-    af_rows_kernel<M, KIND, WGT><<<grid, pl.threads, pl.smem, st>>>(rp);
+    rp.smem_bytes = (int)smem;
+    af_rows_kernel<M, KIND, WGT><<<grid, pl.threads, smem, st>>>(rp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -504,6 +544,7 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
   if (loss && !partials) return fail(GRAF_EINVAL, "loss given but partials is NULL");
   Plan pl = make_plan(af, loss, Kind::Forward);
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
+  if (reinterpret_cast<uintptr_t>(surface) & 15u) pl.bulk_ok = false;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
@@ -538,6 +579,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   if (!aligned8(grad)) return fail(GRAF_EINVAL, "grad is not 8-byte aligned");
   Plan pl = make_plan(af, loss, Kind::LossGrad);
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
+  if (reinterpret_cast<uintptr_t>(surface) & 15u) pl.bulk_ok = false;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");

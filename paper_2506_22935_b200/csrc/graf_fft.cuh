@@ -216,6 +216,13 @@ struct Twiddles {
   static constexpr int NB = tw_offset(M, E, NP);          // base twiddles per thread
   static constexpr int NTW = tw_count(M, E);              // all twiddles per thread
   static constexpr bool CACHE = (NTW > 0 && NTW <= 16);   // keep every power in registers
+  // pass-1 powers from a shared-memory table tw1[(r - 1) * NS1 + jm] (NS1 = first radix;
+  // every thread of a slot shares the NS1 rows, so reads are broadcast / conflict-free)
+  static constexpr bool SMEM1 = !CACHE && NP >= 2;
+  static constexpr int NS1 = NP >= 2 ? pass_ns(M, E, 1) : 1;
+  static constexpr int R1 = NP >= 2 ? pass_radix(M, E, 1) : 1;
+  static constexpr int TAB1 = SMEM1 ? (R1 - 1) * NS1 : 0;   // table entries
+  const float2* tab1 = nullptr;
 #ifdef GRAF_HOLD_BASES
   float2 base[NB > 0 && !CACHE ? NB : 1];
 #endif
@@ -239,6 +246,16 @@ struct Twiddles {
           base[tw_offset(M, E, p) + q] = w1;
 #endif
         }
+      }
+    }
+  }
+
+  // fill the pass-1 table (all threads of the CTA, before the CTA barrier)
+  __device__ __forceinline__ static void fill_tab1(float2* tab, int tid, int nthreads) {
+    if constexpr (SMEM1) {
+      for (int i = tid; i < TAB1; i += nthreads) {
+        const int r = i / NS1 + 1, jm = i % NS1;
+        tab[i] = g_tw[(jm * r * (M / (NS1 * R1))) * (kMaxM / M)];
       }
     }
   }
@@ -267,7 +284,14 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[q + r * Q];
     if constexpr (NS > 1) {
-      if constexpr (Twiddles<M, E>::CACHE) {
+      if constexpr (P == 1 && Twiddles<M, E>::SMEM1) {
+        const float2* tb = tw.tab1 + ((t + q * T) & (NS - 1));
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const float2 w = tb[(r - 1) * NS];
+          x[r] = INV ? cmulc(x[r], w) : cmul(x[r], w);
+        }
+      } else if constexpr (Twiddles<M, E>::CACHE) {
         constexpr int off = tw_count_before(M, E, P);
 #pragma unroll
         for (int r = 1; r < R; ++r) {

@@ -55,6 +55,10 @@ struct RowParams {
   double* part;        // [B][P][kPart]
   float2* gpart;       // [B][P][N]
   const float2* s_pad; // [B][N+M] zero-padded s (global-memory path, M > 8192)
+  int bulk;            // surface rows staged in shared memory + bulk async copies: 1 dedicated
+                       // buffer (stg_floats per slot), 2 aliased to the slot's exchange buffer
+  int stg_floats;      // staging floats per row slot (2*M*{1,2}: rows +k and -k)
+  int smem_bytes;      // dynamic shared memory of the launch (the pass-1 twiddle table ends it)
 };
 
 template <int M>
@@ -222,6 +226,13 @@ __device__ __forceinline__ void lse_merge(double& m, double& Z, double m2, doubl
   }
 }
 
+// sqrt through the MUFU unit (sqrt.approx: ~1 ulp-scale relative error, sqrt(0) = 0)
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // float exp(x) for x <= 0 through the MUFU ex2 unit (rel. error ~2 ulp)
 __device__ __forceinline__ float exp_fast(float x) { return exp2f(x * 1.4426950408889634f); }
 
@@ -297,6 +308,62 @@ __device__ __forceinline__ void row_fft(float2 (&v)[E], float2* sh, int t, const
   }
 }
 
+// ---- bulk asynchronous shared -> global row stores (the TMA engine's 1-D bulk
+// copy; no tensor map).  The surface epilogue stages each finished row in shared
+// memory at its final column order and one thread per row slot hands it to the
+// copy engine, so the HBM stream runs beside the next row's FFT instead of
+// through the LSU pipe as 4-byte stores.
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// slots per batch of predicated accumulator loads in the correlation (loads of a
+// batch are issued back to back, then the stores)
+#ifndef GRAF_CORR_CHUNK
+#define GRAF_CORR_CHUNK 8   // must divide E
+#endif
+constexpr int kCorrChunk = GRAF_CORR_CHUNK;
+
+// predicated shared-memory accesses: a false predicate skips the access (the load
+// returns 0) without a branch
+template <int OFF>
+__device__ __forceinline__ float2 ld_shared_if(unsigned a, bool q) {
+  float2 r;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+      " @q ld.shared.v2.f32 {%0, %1}, [%2+%4];\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(a), "r"((int)q), "n"(OFF)
+      : "memory");
+  return r;
+}
+template <int OFF>
+__device__ __forceinline__ void st_shared_if(unsigned a, float2 v, bool q) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.shared.v2.f32 [%0+%4], {%1, %2};\n}" ::"r"(a),
+               "f"(v.x), "f"(v.y), "r"((int)q), "n"(OFF)
+               : "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// compile-time loop helper: f(integral_constant<int, I>) for I in [B, E)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
 // bits e of [e_lo, e_hi) as a mask over the E register slots
 __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi) {
   const unsigned long long hi = e_hi >= 64 ? ~0ull : ((1ull << e_hi) - 1ull);
@@ -332,6 +399,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   float2* gacc_sh = xch + S * XS;
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
   float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * N : p.gpart + ((size_t)b * P + pb) * N;
+  // surface staging (bulk path): after the gradient accumulators, 16-byte aligned
+  float* stg = reinterpret_cast<float*>(
+                   xch + (((size_t)S * XS + (GRAD && C::G_SMEM ? (size_t)S * N : 0) + 1) & ~(size_t)1)) +
+               (size_t)slot * p.stg_floats;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
   if constexpr (C::S_SMEM) {
@@ -351,9 +422,17 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   }
   Twiddles<C::MX, E2> tw;
   tw.init(t0);
+  // pass-1 twiddle table: the last TAB1 float2 of the dynamic allocation (host adds it)
+  if constexpr (Twiddles<C::MX, E2>::SMEM1) {
+    float2* tab = reinterpret_cast<float2*>(reinterpret_cast<char*>(smem_raw) + p.smem_bytes) -
+                  Twiddles<C::MX, E2>::TAB1;
+    Twiddles<C::MX, E2>::fill_tab1(tab, threadIdx.x, THREADS);
+    tw.tab1 = tab;
+  }
   const float2 wt = SPLIT ? g_tw[t0 * (kMaxM / M)] : make_float2(1.f, 0.f);  // W_M^t (split stage)
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
   using Mask = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
+  using VMask = Mask;
   Mask band = 0, mlb = 0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -386,6 +465,15 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
 
   SlotSync<T, S> sync{1 + slot};
   float2* sh = xch + (size_t)slot * XS;
+  // aliased staging (p.bulk == 2): the row lives in the slot's exchange buffer, which
+  // is free between the last pass of one FFT and the first exchange of the next
+  if (p.bulk == 2) stg = reinterpret_cast<float*>(sh);
+  auto stg_release = [&]() {   // before an FFT reuses an aliased staging buffer
+    if (p.bulk == 2) {
+      if (t0 == 0) bulk_wait_read_all();
+      sync();
+    }
+  };
 
   // per-thread accumulators (double across rows, float within a row)
   double accS = 0.0, accZ = 0.0, accC = 0.0, accF = 0.0;
@@ -404,7 +492,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
     const int lo = k > 0 ? k : 0;
     const int hi = k < 0 ? N + k : N;
     // slots e whose time index n lies in the row's support [lo, hi)
-    unsigned long long vmask;
+    VMask vmask;
     if constexpr (!SPLIT) {
       vmask = slot_range_mask(lo > t ? (lo - t + T - 1) >> LT : 0, hi > t ? (hi - t + T - 1) >> LT : 0);
     } else {
@@ -441,11 +529,70 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
         }
       }
       // ---- a2: forward Doppler FFT
+      stg_release();
       row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
       asm volatile("" ::: "memory");
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
-      if (wpos || wneg) {
+      if (p.bulk) {
+        // dedicated staging: the slot's previous bulk copies must have finished reading it
+        if (p.bulk == 1) {
+          if (t0 == 0) bulk_wait_read_all();
+          sync();
+        }
+        // Rows are staged in natural frequency order: row +k at q = m, row -k at
+        // q = (-m) mod M (A[-k, -m] from A[k, m]); the Doppler layout is applied by
+        // the copies (centred: the two halves swap).  Only slot e = 0 can hold m = 0,
+        // so every other slot's staging address is affine in t.
+        bool wr = wpos || wneg;
+        if constexpr (T < 32) wr = __any_sync(0xffffffffu, wr);   // slot syncs below are warp-wide
+        if (wr) {
+          const float nrm = p.norm_out ? invE : 1.f;
+          if (p.out_kind == GRAF_OUT_C64) {
+            float2* sp = reinterpret_cast<float2*>(stg);
+            float2* sn = sp + M;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int m = t + e * T;
+              if (wpos) sp[m] = cscale(v[e], nrm);
+              if (wneg) {
+                const float2 w = g_tw[(int)(((long long)m * k) & (M - 1)) * (kMaxM / M)];
+                sn[e == 0 ? (M - t) & (M - 1) : M - t - e * T] = cscale(cconj(cmulc(v[e], w)), nrm);
+              }
+            }
+          } else {
+            const bool absk = p.out_kind == GRAF_OUT_ABS_F32;
+            const float sc = absk ? nrm : nrm * nrm;
+            float* sp = stg;
+            float* sn = stg + M;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+              const float val = (absk ? sqrt_approx(chi) : chi) * sc;
+              if (wpos) sp[t + e * T] = val;
+              if (wneg) sn[e == 0 ? (M - t) & (M - 1) : M - t - e * T] = val;
+            }
+          }
+          fence_async_shared();
+          sync();
+          if (t0 == 0 && (wpos || wneg)) {
+            const unsigned rb = (unsigned)(p.stg_floats / 2) * 4u;   // bytes per staged row
+            const char* sp = reinterpret_cast<const char*>(stg);
+            char* out = reinterpret_cast<char*>(p.surface);
+            auto put = [&](char* dst, const char* src) {
+              if (lay) {   // centred: column c <- q = (c - M/2) mod M
+                bulk_store(dst, src + rb / 2, rb / 2);
+                bulk_store(dst + rb / 2, src, rb / 2);
+              } else {
+                bulk_store(dst, src, rb);
+              }
+            };
+            if (wpos) put(out + ((size_t)b * surf_rows + (k - p.kb)) * rb, sp);
+            if (wneg) put(out + ((size_t)b * surf_rows + (-k - p.kb)) * rb, sp + rb);
+            bulk_commit();
+          }
+        }
+      } else if (wpos || wneg) {
         const float nrm = p.norm_out ? invE : 1.f;
         // column of frequency m in row +k: (m + lay) mod M; in row -k: (lay - m) mod M
         if (p.out_kind == GRAF_OUT_C64) {
@@ -472,50 +619,50 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
           for (int e = 0; e < E; ++e) {
             const int m = t + e * T;
             const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-            const float val = (absk ? (chi > 0.f ? chi * rsqrtf(chi) : 0.f) : chi) * sc;
+            const float val = (absk ? sqrt_approx(chi) : chi) * sc;
             if (wpos) __stcs(rp + t + (e < E / 2 ? e * T + lay : e * T - lay), val);
             if (wneg) __stcs(rn + ((lay - m) & (M - 1)), val);
           }
         }
       }
 
-      // ---- a3L (+ a5): loss partials and the cotangent
+      // ---- a3L (+ a5): loss partials and the cotangent.  Branch-free over the
+      //      slots: out-of-region slots select 0 (never multiply: exp of an
+      //      out-of-region value may overflow).
       if (lrow) {
         const Mask inm = band & ~(k <= p.ml_k ? mlb : (Mask)0);
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
         float rowS = 0.f, rowM = -INFINITY, rowF = 0.f;
+        const float gsc = scaleG * mult;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          if (inm & ((Mask)1 << e)) {
-            float w = 1.f;
-            if constexpr (WGT) {
-              const int m = t + e * T;
-              const int d = m < M / 2 ? m : m - M;
-              w = wk * (p.w_d ? p.w_d[d + M / 2] : 1.f);
-            }
-            const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-            rowS = fmaf(w, chi, rowS);
-            if constexpr (KIND == K_FWD) {
-              rowM = fmaxf(rowM, p.normalize ? chi * invE2 : chi);
+          const bool in = (inm >> e) & 1;
+          float w = 1.f;
+          if constexpr (WGT) {
+            const int m = t + e * T;
+            const int d = m < M / 2 ? m : m - M;
+            w = wk * (p.w_d ? p.w_d[d + M / 2] : 1.f);
+          }
+          const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+          rowS = fmaf(in ? w : 0.f, chi, rowS);
+          if constexpr (KIND == K_FWD) {
+            rowM = fmaxf(rowM, in ? (p.normalize ? chi * invE2 : chi) : -INFINITY);
+          } else if constexpr (KIND == K_ISL) {
+            v[e] = cscale(v[e], in ? p.lam_isl * w * gsc : 0.f);   // G (x2 for a folded row pair)
+          } else {
+            const float x = p.normalize ? chi * invE2 : chi;
+            float fp;
+            if (use_centred) {
+              fp = p.lam_psl * (expm1_fast((x - p.xbar) * p.invT) - ebar) * invZc;
             } else {
-              float fp;
-              if constexpr (KIND == K_ISL) {
-                fp = p.lam_isl * w;
-              } else {
-                const float x = p.normalize ? chi * invE2 : chi;
-                if (use_centred) {
-                  fp = p.lam_psl * (expm1_fast((x - p.xbar) * p.invT) - ebar) * invZc;
-                } else {
-                  fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);
-                }
-              }
-              rowF = fmaf(fp, chi, rowF);
-              v[e] = cscale(v[e], fp * scaleG * mult);   // G (x2 for a folded row pair)
+              fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);
             }
-          } else if constexpr (GRAD) {
-            v[e] = make_float2(0.f, 0.f);
+            fp = in ? fp : 0.f;
+            rowF = fmaf(fp, chi, rowF);
+            v[e] = cscale(v[e], fp * gsc);
           }
         }
+        if constexpr (KIND == K_ISL) rowF = p.lam_isl * rowS;
         accS += (double)(mult * rowS);
         accF += (double)(mult * rowF);
         if constexpr (KIND == K_FWD) {
@@ -527,11 +674,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
             float rowZ = 0.f, rowC = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-              if (inm & ((Mask)1 << e)) {
-                const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-                const float x = p.normalize ? chi * invE2 : chi;
-                rowZ += exp_fast((x - accM) * p.invT);
-                if (p.centred) rowC += expm1_fast((x - p.xbar) * p.invT);
+              const bool in = (inm >> e) & 1;
+              const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+              const float x = p.normalize ? chi * invE2 : chi;
+              const float z = exp_fast((x - accM) * p.invT);
+              rowZ += in ? z : 0.f;
+              if (p.centred) {
+                const float c = expm1_fast((x - p.xbar) * p.invT);
+                rowC += in ? c : 0.f;
               }
             }
             accZ += (double)(mult * rowZ);
@@ -558,29 +708,51 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
       bool do_adj = lrow;
       if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
       if (do_adj) {
+        stg_release();
         row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
         // keep the correlation's loads below the last inverse pass
         asm volatile("" ::: "memory");
         // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n],
         // for n in the row's support (vmask); each address is touched once per phase.
-        const unsigned long long m1 = lrow ? vmask : 0ull;
+        const VMask m1 = lrow ? vmask : (VMask)0;
         // time offset of slot e relative to the thread's base index
-        auto toff = [](int e) { return SPLIT ? (e < E2 ? 2 * e * T : 2 * (e - E2) * T + 1) : e * T; };
+        constexpr auto toff = [](int e) constexpr { return SPLIT ? (e < E2 ? 2 * e * T : 2 * (e - E2) * T + 1) : e * T; };
         const int tb = SPLIT ? 2 * t : t;
+        // predicated shared-memory read-modify-writes (no branches; an out-of-support
+        // slot neither loads nor stores its accumulator)
+        constexpr int CC = E < kCorrChunk ? E : kCorrChunk;
         {
-          float2* g1 = gacc + tb;
+          const unsigned g1 = smem_u32(gacc + tb);
           const float2* s1 = sv + tb - k;
-#pragma unroll
-          for (int e = 0; e < E; ++e)
-            if (m1 & (1ull << e)) g1[toff(e)] = cadd(g1[toff(e)], cmul(v[e], s1[toff(e)]));
+          static_for<0, E / CC>([&](auto c) {
+            constexpr int e0 = decltype(c)::value * CC;
+            float2 a[CC];
+            static_for<0, CC>([&](auto i) {
+              constexpr int e = e0 + decltype(i)::value;
+              a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g1, (m1 >> e) & 1);
+            });
+            static_for<0, CC>([&](auto i) {
+              constexpr int e = e0 + decltype(i)::value;
+              st_shared_if<8 * toff(e)>(g1, cadd(a[decltype(i)::value], cmul(v[e], s1[toff(e)])), (m1 >> e) & 1);
+            });
+          });
         }
         sync();
         {
-          float2* g2 = gacc + tb - k;
+          const unsigned g2 = smem_u32(gacc + tb - k);
           const float2* s2 = sv + tb;
-#pragma unroll
-          for (int e = 0; e < E; ++e)
-            if (m1 & (1ull << e)) g2[toff(e)] = cadd(g2[toff(e)], cmulc(s2[toff(e)], v[e]));
+          static_for<0, E / CC>([&](auto c) {
+            constexpr int e0 = decltype(c)::value * CC;
+            float2 a[CC];
+            static_for<0, CC>([&](auto i) {
+              constexpr int e = e0 + decltype(i)::value;
+              a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g2, (m1 >> e) & 1);
+            });
+            static_for<0, CC>([&](auto i) {
+              constexpr int e = e0 + decltype(i)::value;
+              st_shared_if<8 * toff(e)>(g2, cadd(a[decltype(i)::value], cmulc(s2[toff(e)], v[e])), (m1 >> e) & 1);
+            });
+          });
         }
         sync();
       }
@@ -588,6 +760,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_
   }
 
   // ---- CTA reduction of the scalar partials -> part[b][pb]
+  if (p.bulk && t0 == 0) bulk_wait_all();
   __syncthreads();
   double* scratch = reinterpret_cast<double*>(xch);  // exchange space is free now
   double* rec = p.part + ((size_t)b * P + pb) * kPart;

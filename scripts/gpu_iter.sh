@@ -1,0 +1,12 @@
+#!/bin/bash
+# One development iteration on the GPU box: parity tests, then every bench line.
+# Usage (under gpurun): [SKIP_TESTS=1] bash scripts/gpu_iter.sh <tag> [configs...]
+TAG=$1; shift; CFGS=${@:-2 3 4 5}
+mkdir -p gpurun_out
+if [ -z "$SKIP_TESTS" ]; then
+  timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/tests_$TAG.log 2>&1
+  echo "tests exit=$?"; tail -3 gpurun_out/tests_$TAG.log
+fi
+bash scripts/bench_all.sh $TAG $CFGS
+timeout 600 python bench.py --config 3 --mode forward --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c3fwd.json 2> gpurun_out/bench_${TAG}_c3fwd.err
+python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c3fwd.json')); r=d['roofline']; print('c3fwd', d['ms_per_step'], r['bound'], r['frac'])"
