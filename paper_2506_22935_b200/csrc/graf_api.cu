@@ -221,7 +221,11 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   if (kind != Kind::Backward && af->out_kind != GRAF_OUT_NONE) {
     const size_t row_bytes = (size_t)af->m * (af->out_kind == GRAF_OUT_C64 ? 8 : 4);
     // the copies move whole rows (raw) or half rows (centred) in 16-byte units
+#ifndef GRAF_NO_BULK
     if ((af->doppler_layout == GRAF_DOPPLER_CENTERED ? row_bytes / 2 : row_bytes) % 16 == 0) {
+#else
+    if (false) {
+#endif
       pl.bulk_ok = true;
       pl.stg_floats = (int)(2 * row_bytes / 4);
       pl.smem_stg = (size_t)ci.S * 2 * row_bytes + 16;

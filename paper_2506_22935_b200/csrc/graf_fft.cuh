@@ -124,9 +124,12 @@ __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x
 
 // exchange-buffer padding: one pad slot every max-radix elements (conflict-free
 // for every plan used; scripts/bank_sim.py)
+#ifndef GRAF_MAX_RADIX
+#define GRAF_MAX_RADIX 32
+#endif
 template <int E>
 struct Pad {
-  static constexpr int P = E > 16 ? 16 : E;     // pad period
+  static constexpr int P = E > GRAF_MAX_RADIX ? GRAF_MAX_RADIX : E;   // pad period = max radix
   static constexpr int S = ilog2(P);
 };
 template <int E>
@@ -150,9 +153,8 @@ __device__ __forceinline__ int launder(int x) {
 }
 
 // ---- compile-time pass plan: radices RM, RM, ..., remainder (GRAF_REM_FIRST=1
-// puts the remainder first), with RM = min(E, 16) (a thread with E = 32 values
-// runs two radix-16 butterflies per pass)
-__host__ __device__ constexpr int max_radix(int E) { return E > 16 ? 16 : E; }
+// puts the remainder first), with RM = min(E, GRAF_MAX_RADIX)
+__host__ __device__ constexpr int max_radix(int E) { return E > GRAF_MAX_RADIX ? GRAF_MAX_RADIX : E; }
 __host__ __device__ constexpr int first_radix(int M, int E) {
   int m = M;
   while (m >= max_radix(E)) m /= max_radix(E);
@@ -284,7 +286,7 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[q + r * Q];
     if constexpr (NS > 1) {
-      if constexpr (P == 1 && Twiddles<M, E>::SMEM1) {
+      if (P == 1 && Twiddles<M, E>::SMEM1 && tw.tab1) {
         const float2* tb = tw.tab1 + ((t + q * T) & (NS - 1));
 #pragma unroll
         for (int r = 1; r < R; ++r) {

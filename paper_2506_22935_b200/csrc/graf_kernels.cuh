@@ -74,7 +74,7 @@ struct Cfg;
     static constexpr int THREADS = T * S;                            \
     static constexpr bool SPLIT = (M_ >= 16384);                     \
     static constexpr int MX = SPLIT ? M_ / 2 : M_;  /* exchanged FFT length */ \
-    static constexpr int XS = MX + MX / ((SPLIT ? E_ / 2 : E_) > 16 ? 16 : (SPLIT ? E_ / 2 : E_)); \
+    static constexpr int XS = MX + MX / Pad<SPLIT ? E_ / 2 : E_>::P;  /* padded exchange */ \
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
     static constexpr bool G_SMEM = true;                             \
   };
@@ -104,10 +104,10 @@ struct Cfg;
 #define GRAF_S_512 2
 #endif
 #ifndef GRAF_E_1024
-#define GRAF_E_1024 16
+#define GRAF_E_1024 32
 #endif
 #ifndef GRAF_S_1024
-#define GRAF_S_1024 2
+#define GRAF_S_1024 4
 #endif
 #ifndef GRAF_E_2048
 #define GRAF_E_2048 16
@@ -246,12 +246,14 @@ __device__ __forceinline__ float expm1_fast(float u) {
 
 // minimum resident CTAs per SM requested from ptxas (caps registers per thread);
 // a tuning build may force one value for every size with -DGRAF_MINB=..
-template <int M>
+// (measured on B200, scripts/tune.py: M = 1024 runs E = 32 radix-32 passes, one
+// exchange per FFT; 3 CTAs/SM for the forward pass, 2 for the gradient kernels)
+template <int M, int KIND>
 struct MinBlocks {
 #ifdef GRAF_MINB
   static constexpr int value = GRAF_MINB;
 #else
-  static constexpr int value = M <= 16 ? 2 : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
+  static constexpr int value = M <= 16 ? 2 : M == 1024 ? (KIND == 0 ? 3 : 2) : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
 #endif
 };
 // radix-2 split stage between the two M/2-point halves (twiddle W_M^{t + e T} =
@@ -372,7 +374,7 @@ __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi
 }
 
 template <int M, int KIND, bool WGT>
-__global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M>::value) af_rows_kernel(RowParams p) {
+__global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
   constexpr int LT = ilog2(T);

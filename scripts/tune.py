@@ -58,8 +58,13 @@ def one(lib, cfg, steps=30):
         surf = torch.empty((B, 2 * N - 1, M), dtype=torch.complex64 if out == "c64" else torch.float32,
                            device="cuda")
 
+    fwd = os.environ.get("GRAF_TUNE_MODE") == "forward"
+
     def call():
-        graf.af_loss_grad(s, M, spec, out=out, ws=ws, grad=grad, loss_out=lo, surface=surf, stream=st)
+        if fwd:
+            graf.af_forward(s, M, out=out, layout="centered", ws=ws, surface=surf, stream=st)
+        else:
+            graf.af_loss_grad(s, M, spec, out=out, ws=ws, grad=grad, loss_out=lo, surface=surf, stream=st)
 
     with torch.cuda.stream(st):
         call()
@@ -80,7 +85,8 @@ def one(lib, cfg, steps=30):
             if i >= 5:
                 ts.append(a.elapsed_time(b))
     ts.sort()
-    res = {"lib": os.path.basename(lib), "median_ms": ts[len(ts) // 2], "min_ms": ts[0],
+    chk = float(surf.float().abs().sum().item()) if (fwd and surf is not None) else None
+    res = {"lib": os.path.basename(lib), "median_ms": ts[len(ts) // 2], "min_ms": ts[0], "surf_abs_sum": chk,
            "loss0": lo[0].item(), "gmax": grad.abs().max().item(), "g00": [grad[0, 0].real.item(), grad[0, 0].imag.item()]}
     print(json.dumps(res))
 
