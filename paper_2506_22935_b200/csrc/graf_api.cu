@@ -79,6 +79,10 @@ struct Plan {
   bool bulk_ok = false, alias_ok = false;
   size_t smem_stg = 0;
   int bulk_mode = -1;   // decided at the first launch of a call: 0 direct, 1 dedicated, 2 alias
+  // left-padded gradient accumulators (M == N loss calls), if they cost no resident CTA
+  bool gpad_ok = false;
+  size_t smem_gpad = 0;
+  int gpad_mode = -1;
   size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
 };
 
@@ -218,6 +222,10 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   }
   pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? (size_t)ci.S * N : 0) + (size_t)ci.tab1);
+  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem) {
+    pl.gpad_ok = true;
+    pl.smem_gpad = sizeof(float2) * (size_t)ci.S * N;
+  }
   if (kind != Kind::Backward && af->out_kind != GRAF_OUT_NONE) {
     const size_t row_bytes = (size_t)af->m * (af->out_kind == GRAF_OUT_C64 ? 8 : 4);
     // the copies move whole rows (raw) or half rows (centred) in 16-byte units
@@ -297,13 +305,29 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   if (e0 != cudaSuccess) return e0;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   size_t smem = pl.smem;
+  rp.gpad = 0;
+  if (pl.gpad_ok && KIND != K_ADJ && KIND != K_FWD) {
+    if (pl.gpad_mode < 0) {
+      int occ_g = 0;
+      const bool fits = pl.smem + pl.smem_gpad <= 227 * 1024;
+      if (fits) {
+        e0 = kernel_occupancy<M, KIND, WGT>(pl.smem + pl.smem_gpad, &occ_g, &nsm);
+        if (e0 != cudaSuccess) return e0;
+      }
+      pl.gpad_mode = (fits && occ_g >= occ) ? 1 : 0;
+    }
+    if (pl.gpad_mode == 1) {
+      rp.gpad = 1;
+      smem += pl.smem_gpad;
+    }
+  }
   if (rp.surface && pl.bulk_ok) {
     if (pl.bulk_mode < 0) {
       // dedicated staging unless it costs resident CTAs and the exchange buffer can hold the rows
       int occ_d = 0;
-      const bool fits = pl.smem + pl.smem_stg <= 227 * 1024;
+      const bool fits = smem + pl.smem_stg <= 227 * 1024;
       if (fits) {
-        e0 = kernel_occupancy<M, KIND, WGT>(pl.smem + pl.smem_stg, &occ_d, &nsm);
+        e0 = kernel_occupancy<M, KIND, WGT>(smem + pl.smem_stg, &occ_d, &nsm);
         if (e0 != cudaSuccess) return e0;
       }
       pl.bulk_mode = (fits && (occ_d >= occ || !pl.alias_ok) && occ_d >= 1) ? 1 : pl.alias_ok ? 2 : 0;

@@ -58,6 +58,7 @@ struct RowParams {
   int bulk;            // surface rows staged in shared memory + bulk async copies: 1 dedicated
                        // buffer (stg_floats per slot), 2 aliased to the slot's exchange buffer
   int stg_floats;      // staging floats per row slot (2*M*{1,2}: rows +k and -k)
+  int gpad;            // 1: left-padded gradient accumulators (M == N, folded rows)
   int smem_bytes;      // dynamic shared memory of the launch (the pass-1 twiddle table ends it)
 };
 
@@ -400,10 +401,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   float2* xch = s_pad + (C::S_SMEM ? NP2 : 0);
   float2* gacc_sh = xch + S * XS;
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
-  float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * N : p.gpart + ((size_t)b * P + pb) * N;
+  // per-slot accumulator stride: N, or 2N with N zero-padding on the left (p.gpad: folded
+  // rows with M == N need no support predicates, out-of-support terms land in the pad)
+  const int GS = p.gpad ? 2 * N : N;
+  float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * GS + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
   // surface staging (bulk path): after the gradient accumulators, 16-byte aligned
   float* stg = reinterpret_cast<float*>(
-                   xch + (((size_t)S * XS + (GRAD && C::G_SMEM ? (size_t)S * N : 0) + 1) & ~(size_t)1)) +
+                   xch + (((size_t)S * XS + (GRAD && C::G_SMEM ? (size_t)S * GS : 0) + 1) & ~(size_t)1)) +
                (size_t)slot * p.stg_floats;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   }
   if constexpr (GRAD) {
     if constexpr (C::G_SMEM) {
-      for (int i = threadIdx.x; i < S * N; i += THREADS) gacc_sh[i] = make_float2(0.f, 0.f);
+      for (int i = threadIdx.x; i < S * GS; i += THREADS) gacc_sh[i] = make_float2(0.f, 0.f);
     } else {
       for (int i = threadIdx.x; i < N; i += THREADS) gacc[i] = make_float2(0.f, 0.f);
     }
@@ -722,39 +726,58 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const int tb = SPLIT ? 2 * t : t;
         // predicated shared-memory read-modify-writes (no branches; an out-of-support
         // slot neither loads nor stores its accumulator)
-        constexpr int CC = E < kCorrChunk ? E : kCorrChunk;
-        {
-          const unsigned g1 = smem_u32(gacc + tb);
-          const float2* s1 = sv + tb - k;
-          static_for<0, E / CC>([&](auto c) {
-            constexpr int e0 = decltype(c)::value * CC;
-            float2 a[CC];
-            static_for<0, CC>([&](auto i) {
-              constexpr int e = e0 + decltype(i)::value;
-              a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g1, (m1 >> e) & 1);
+        if (KIND != K_ADJ && p.gpad) {
+          // M == N, k >= 0: every term-1 position n < N is in the slot's range and
+          // s[n - k] = 0 below the support; term-2 positions n - k >= -k land in the
+          // left pad when n < k.  No predicates.
+          {
+            float2* g1 = gacc + tb;
+            const float2* s1 = sv + tb - k;
+#pragma unroll
+            for (int e = 0; e < E; ++e) g1[toff(e)] = cadd(g1[toff(e)], cmul(v[e], s1[toff(e)]));
+          }
+          sync();
+          {
+            float2* g2 = gacc + tb - k;
+            const float2* s2 = sv + tb;
+#pragma unroll
+            for (int e = 0; e < E; ++e) g2[toff(e)] = cadd(g2[toff(e)], cmulc(s2[toff(e)], v[e]));
+          }
+        } else {
+          constexpr int CC = E < kCorrChunk ? E : kCorrChunk;
+          {
+            const unsigned g1 = smem_u32(gacc + tb);
+            const float2* s1 = sv + tb - k;
+            static_for<0, E / CC>([&](auto c) {
+              constexpr int e0 = decltype(c)::value * CC;
+              float2 a[CC];
+              static_for<0, CC>([&](auto i) {
+                constexpr int e = e0 + decltype(i)::value;
+                a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g1, (m1 >> e) & 1);
+              });
+              static_for<0, CC>([&](auto i) {
+                constexpr int e = e0 + decltype(i)::value;
+                st_shared_if<8 * toff(e)>(g1, cadd(a[decltype(i)::value], cmul(v[e], s1[toff(e)])), (m1 >> e) & 1);
+              });
             });
-            static_for<0, CC>([&](auto i) {
-              constexpr int e = e0 + decltype(i)::value;
-              st_shared_if<8 * toff(e)>(g1, cadd(a[decltype(i)::value], cmul(v[e], s1[toff(e)])), (m1 >> e) & 1);
+          }
+          sync();
+          {
+            const unsigned g2 = smem_u32(gacc + tb - k);
+            const float2* s2 = sv + tb;
+            static_for<0, E / CC>([&](auto c) {
+              constexpr int e0 = decltype(c)::value * CC;
+              float2 a[CC];
+              static_for<0, CC>([&](auto i) {
+                constexpr int e = e0 + decltype(i)::value;
+                a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g2, (m1 >> e) & 1);
+              });
+              static_for<0, CC>([&](auto i) {
+                constexpr int e = e0 + decltype(i)::value;
+                st_shared_if<8 * toff(e)>(g2, cadd(a[decltype(i)::value], cmulc(s2[toff(e)], v[e])), (m1 >> e) & 1);
+              });
             });
-          });
-        }
-        sync();
-        {
-          const unsigned g2 = smem_u32(gacc + tb - k);
-          const float2* s2 = sv + tb;
-          static_for<0, E / CC>([&](auto c) {
-            constexpr int e0 = decltype(c)::value * CC;
-            float2 a[CC];
-            static_for<0, CC>([&](auto i) {
-              constexpr int e = e0 + decltype(i)::value;
-              a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g2, (m1 >> e) & 1);
-            });
-            static_for<0, CC>([&](auto i) {
-              constexpr int e = e0 + decltype(i)::value;
-              st_shared_if<8 * toff(e)>(g2, cadd(a[decltype(i)::value], cmulc(s2[toff(e)], v[e])), (m1 >> e) & 1);
-            });
-          });
+          }
         }
         sync();
       }
@@ -800,9 +823,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   if constexpr (GRAD && C::G_SMEM) {
     float2* gout = p.gpart + ((size_t)b * P + pb) * N;
     for (int n = threadIdx.x; n < N; n += THREADS) {
-      float2 a = gacc_sh[n];
+      const float2* g0 = gacc_sh + (p.gpad ? N : 0) + n;
+      float2 a = g0[0];
 #pragma unroll 1
-      for (int sl = 1; sl < S; ++sl) a = cadd(a, gacc_sh[(size_t)sl * N + n]);
+      for (int sl = 1; sl < S; ++sl) a = cadd(a, g0[(size_t)sl * GS]);
       gout[n] = a;
     }
   }

@@ -8,3 +8,8 @@ echo "plain $TAG exit=$?"; cat gpurun_out/plain_${TAG}.json | python -c "import 
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$KRE -s $SKIP -c 1 \
   -o gpurun_out/prof_${TAG} python bench.py --config $CFG $EXTRA --steps 1 --warmup 3 --no-cpu-baseline --settle-s 0 > gpurun_out/ncu_${TAG}.log 2>&1
 echo "ncu $TAG exit=$?"
+# summarise on the box (reports of the big kernels exceed gpurun's 64 MiB return limit)
+python scripts/ncu_summary.py gpurun_out/prof_${TAG}.ncu-rep gpurun_out/sum_${TAG}.txt > /dev/null 2>&1
+python scripts/ncu_mix.py gpurun_out/prof_${TAG}.ncu-rep > gpurun_out/mix_${TAG}.txt 2>&1
+SZ=$(stat -c %s gpurun_out/prof_${TAG}.ncu-rep 2>/dev/null || echo 0)
+if [ "$SZ" -gt 25000000 ]; then rm -f gpurun_out/prof_${TAG}.ncu-rep; fi
