@@ -83,6 +83,8 @@ struct Plan {
   bool gpad_ok = false;
   size_t smem_gpad = 0;
   int gpad_mode = -1;
+  // fused finalize (K_ISL only): requested by the caller, granted when P <= 8
+  bool fuse_req = false, fused = false;
   size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
 };
 
@@ -222,7 +224,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   }
   pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? (size_t)ci.S * N : 0) + (size_t)ci.tab1);
-  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem) {
+  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512) {
     pl.gpad_ok = true;
     pl.smem_gpad = sizeof(float2) * (size_t)ci.S * N;
   }
@@ -346,11 +348,34 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
     pl.P = choose_P(pl, B, occ, nsm);
     pl.fixedP = true;   // later passes of the same call reuse it
   }
+  rp.fuse = 0;
+  if (KIND == K_ISL && pl.fuse_req && pl.P >= 2 && pl.P <= 8) {   // (P = 1: measured slower as a cluster launch)
+    rp.fuse = 1;
+    pl.fused = true;
+  }
   for (int b0 = 0; b0 < B; b0 += 65535) {
     rp.b0 = b0;
     dim3 grid(pl.P, std::min(65535, B - b0));
     rp.smem_bytes = (int)smem;
-    af_rows_kernel<M, KIND, WGT><<<grid, pl.threads, smem, st>>>(rp);
+    if (rp.fuse) {
+      // the P CTAs of a waveform form one thread-block cluster (rank 0 finalizes)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(pl.threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)pl.P;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, af_rows_kernel<M, KIND, WGT>, rp);
+      if (e != cudaSuccess) return e;
+    } else {
+      af_rows_kernel<M, KIND, WGT><<<grid, pl.threads, smem, st>>>(rp);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -624,7 +649,11 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   graf_partials* comb = reinterpret_cast<graf_partials*>(static_cast<char*>(ws) + pl.off_comb);
   const graf_partials* stats = global;
   if (loss->lambda_psl == 0.f) {
-    // single fused pass (f' = lambda_isl * w known up front)
+    // single fused pass (f' = lambda_isl * w known up front); unsharded calls also
+    // fuse the finalize into the row kernel when a waveform's CTAs fit one cluster
+    pl.fuse_req = (global == nullptr);
+    rp.loss_out = loss_out;
+    rp.grad_out = static_cast<float2*>(grad);
     if (pl.U > 0) {
       prof_mark(true, cs);
       e = launch_rows(pl, rp, (int)af->batch, cs, K_ISL);
@@ -657,6 +686,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     }
     return GRAF_OK;
   }
+  if (pl.fused) return GRAF_OK;
   return run_finalize(af, loss, pl, s, ws, stats, loss_out, grad, true, cs);
 }
 

@@ -20,6 +20,7 @@
 // rows +k and -k (loss sums and gradient terms counted twice; SURVEY §8(c)
 // "symmetric-loss identities").
 #pragma once
+#include <cooperative_groups.h>
 #include <type_traits>
 #include "../../include/graf.h"
 #include "graf_fft.cuh"
@@ -59,6 +60,12 @@ struct RowParams {
                        // buffer (stg_floats per slot), 2 aliased to the slot's exchange buffer
   int stg_floats;      // staging floats per row slot (2*M*{1,2}: rows +k and -k)
   int gpad;            // 1: left-padded gradient accumulators (M == N, folded rows)
+  // fused finalize (K_ISL, P <= 8 CTAs per waveform launched as one thread-block
+  // cluster): cluster rank 0 combines the CTAs' partials over distributed shared
+  // memory and writes loss and grad directly (no partial records, no finalize kernel)
+  int fuse;
+  double* loss_out;    // [B] (nullable)
+  float2* grad_out;    // [B][N]
   int smem_bytes;      // dynamic shared memory of the launch (the pass-1 twiddle table ends it)
 };
 
@@ -403,6 +410,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
   // per-slot accumulator stride: N, or 2N with N zero-padding on the left (p.gpad: folded
   // rows with M == N need no support predicates, out-of-support terms land in the pad)
+  // (compiled for the small sizes only: at M >= 1024 the padded accumulators never fit
+  // beside the resident CTAs the gradient kernels need)
+  constexpr bool kGpadSizes = (M <= 512);
   const int GS = p.gpad ? 2 * N : N;
   float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * GS + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
   // surface staging (bulk path): after the gradient accumulators, 16-byte aligned
@@ -726,7 +736,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const int tb = SPLIT ? 2 * t : t;
         // predicated shared-memory read-modify-writes (no branches; an out-of-support
         // slot neither loads nor stores its accumulator)
-        if (KIND != K_ADJ && p.gpad) {
+        if (KIND != K_ADJ && kGpadSizes && p.gpad) {
           // M == N, k >= 0: every term-1 position n < N is in the slot's range and
           // s[n - k] = 0 below the support; term-2 positions n - k >= -k land in the
           // left pad when n < k.  No predicates.
@@ -784,11 +794,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     }
   }
 
-  // ---- CTA reduction of the scalar partials -> part[b][pb]
+  // ---- CTA reduction of the scalar partials -> part[b][pb] (or, fused, shared memory)
   if (p.bulk && t0 == 0) bulk_wait_all();
   __syncthreads();
   double* scratch = reinterpret_cast<double*>(xch);  // exchange space is free now
-  double* rec = p.part + ((size_t)b * P + pb) * kPart;
+  double* rec = p.fuse ? red + 8 : p.part + ((size_t)b * P + pb) * kPart;
   if constexpr (KIND != K_ADJ) {
     const double S0 = block_sum<THREADS>(accS, scratch);
     const double F0 = block_sum<THREADS>(accF, scratch);
@@ -821,13 +831,51 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 
   // ---- gradient accumulators of all slots -> this CTA's partial g (fixed slot order)
   if constexpr (GRAD && C::G_SMEM) {
-    float2* gout = p.gpart + ((size_t)b * P + pb) * N;
+    float2* gout = p.fuse ? gacc_sh + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
     for (int n = threadIdx.x; n < N; n += THREADS) {
       const float2* g0 = gacc_sh + (p.gpad ? N : 0) + n;
       float2 a = g0[0];
 #pragma unroll 1
       for (int sl = 1; sl < S; ++sl) a = cadd(a, g0[(size_t)sl * GS]);
-      gout[n] = a;
+      gout[n] = a;   // fused: in place over slot 0 (each n is owned by one thread)
+    }
+  }
+
+  // ---- fused finalize over the cluster (SURVEY §8(a) a4 + a7 final, K5)
+  if constexpr (KIND == K_ISL) {
+    if (p.fuse) {
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();   // every CTA's record and combined gradient are visible cluster-wide
+      if (cl.block_rank() == 0) {
+        const float2* gl = gacc_sh + (p.gpad ? N : 0);
+        if (threadIdx.x == 0) {
+          double St = 0.0, Ft = 0.0;
+          for (int r = 0; r < P; ++r) {
+            const double* rr = cl.map_shared_rank(red + 8, r);
+            St += rr[0];
+            Ft += rr[4];
+          }
+          const double Ed = red[0];
+          if (p.loss_out) p.loss_out[b] = (double)p.lam_isl * (p.normalize ? St / (Ed * Ed) : St);
+          red[16] = Ft;
+        }
+        __syncthreads();
+        const double Ed = red[0];
+        const float coef = p.normalize ? (float)(2.0 * red[16] / (Ed * Ed * Ed)) : 0.f;
+        const float2* sg = p.s + (size_t)b * N;
+        for (int n = threadIdx.x; n < N; n += THREADS) {
+          double gx = 0.0, gy = 0.0;
+          for (int r = 0; r < P; ++r) {
+            const float2 a = *cl.map_shared_rank(gl + n, r);
+            gx += a.x;
+            gy += a.y;
+          }
+          const float2 sn = sg[n];
+          p.grad_out[(size_t)b * N + n] = make_float2((float)gx - coef * sn.x, (float)gy - coef * sn.y);
+        }
+      }
+      cl.sync();   // keep every CTA's shared memory alive until rank 0 has read it
     }
   }
 }
