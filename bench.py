@@ -260,7 +260,6 @@ def main():
         from paper_2506_22935_b200 import sharding
         s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=0)).pin_memory()
         s = s_host.to(dev)
-        tb = TimedBackend(graf, sharding)
 
     def call(st=None):
         if delay:
@@ -275,15 +274,29 @@ def main():
     with torch.cuda.stream(stream):
         call(stream)                                    # twiddle init + workspace, before capture
     torch.cuda.synchronize()
+    L = graf.lib()
+    launches_per_step = int(L.graf_last_launch_count())   # device ops the ABI call enqueued
+    # the dominant kernel(s) are bracketed by events the ABI records around its
+    # delay-row kernels (graf_set_profile_events); recorded into the captured graph,
+    # so the kernel time comes from the same graph replays as the step time
+    ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
+    ev_k1.record(stream)
+    torch.cuda.synchronize()
     if delay:
+        tb = TimedBackend(graf, sharding)
         class _Eager:                     # NCCL step: eager replay (no graph)
             def replay(self_inner):
                 call(stream)
         g = _Eager()
     else:
-        g = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph()               # the timed step (no event nodes)
         with torch.cuda.graph(g, stream=stream):
             call(stream)
+        g_k = torch.cuda.CUDAGraph()             # the same call with the kernel events recorded
+        L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
+        with torch.cuda.graph(g_k, stream=stream):
+            call(stream)
+        L.graf_set_profile_events(None, None)
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
@@ -316,9 +329,8 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]
-    # dominant kernel(s): the ABI records ev_k0/ev_k1 around its delay-row kernels
-    # (graf_set_profile_events); eager calls, same inputs, same L2 flush protocol.
-    L = graf.lib()
+    # dominant kernel(s): ev_k0/ev_k1 around the delay-row kernels, same inputs, same
+    # L2 flush protocol (graph replays; eager ABI calls for the NCCL-sharded step)
     if delay:
         with torch.cuda.stream(stream):
             for i in range(args.steps):
@@ -327,17 +339,12 @@ def main():
                 torch.cuda.synchronize()
                 kern_ms.append(tb.kernel_ms())
     else:
-        ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
-        ev_k1.record(stream)
-        torch.cuda.synchronize()
-        L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
         with torch.cuda.stream(stream):
             for i in range(args.steps):
                 flush.zero_()
-                call(stream)
+                g_k.replay()
                 ev_k1.synchronize()
                 kern_ms.append(ev_k0.elapsed_time(ev_k1))
-        L.graf_set_profile_events(None, None)
     total_ms = sum(step_ms)
     kern_avg = sum(kern_ms) / len(kern_ms)
     if world > 1:
@@ -410,7 +417,9 @@ def main():
                 "frac": fl_tf / FP32_PEAK_TFLOPS,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)"}
     roof["traffic"] = read_traffic(w["cid"])
-    roof["kernel"] = f"af_rows_kernel<{M}> (+ pass-1/reduce when soft-PSL)"
+    roof["kernel"] = (f"af_rows_kernel<{M}>" + (" (pass 1 + reduce + pass 2)" if w["loss"]["lambda_psl"] else "")
+                      + (" with the fused cluster finalize" if launches_per_step == 1 and args.mode != "forward"
+                         else ""))
     roof["kernel_ms"] = kern_avg
     roof["algorithmic_flops_per_launch"] = w["flops"]
     roof["algorithmic_bytes_per_launch"] = bytes_k
@@ -439,7 +448,7 @@ def main():
                         "path": ("pinned host s -> H2D -> graf.af_loss_grad (C ABI) -> D2H loss + grad"
                                  if args.mode != "forward" else
                                  "pinned host s -> H2D -> graf.af_forward (C ABI) -> D2H zero-delay cut")},
-                "gpu_launches": (w["launches"] + (1 if delay else 0)) * args.steps,
+                "gpu_launches": ((w["launches"] + 1) if delay else launches_per_step) * args.steps,
                 "clocks": clocks}
         print(json.dumps(line))
     if world > 1:
@@ -481,6 +490,10 @@ class TimedBackend:
 def ctypes_ptr(ev):
     import ctypes
     return ctypes.c_void_p(ev.cuda_event)
+
+
+def ctypes_null():
+    return None
 
 
 if __name__ == "__main__":

@@ -150,6 +150,11 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
                                   int32_t G, int64_t B, graf_partials* out,
                                   int32_t on_device, void* stream);
 
+/* Diagnostics: number of device operations (kernels and memsets) that the calling
+ * thread's most recent entry-point call enqueued (e.g. 1 for a fused single-pass
+ * ISL call whose finalize runs inside the row kernel; 2 when it runs separately). */
+int32_t graf_last_launch_count(void);
+
 /* Diagnostics: with both events non-NULL (cudaEvent_t handles created by the
  * caller), every later entry-point call made by THIS thread records `start` on
  * its stream just before its first delay-row kernel (af_rows_kernel) and `stop`

@@ -17,7 +17,7 @@ DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
 
 EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_workspace_bytes",
            "graf_af_forward", "graf_af_loss_grad", "graf_af_backward", "graf_combine_partials",
-           "graf_set_profile_events")
+           "graf_set_profile_events", "graf_last_launch_count")
 
 
 class AfDesc(ctypes.Structure):
@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         L.graf_combine_partials.restype = c_int32
         L.graf_combine_partials.argtypes = [POINTER(LossDesc), c_void_p, c_int32, c_int64, c_void_p, c_int32,
                                             c_void_p]
+        L.graf_last_launch_count.restype = c_int32
+        L.graf_last_launch_count.argtypes = []
         L.graf_set_profile_events.restype = c_int32
         L.graf_set_profile_events.argtypes = [c_void_p, c_void_p]
         if L.graf_abi_version() != ABI_VERSION:

@@ -17,11 +17,16 @@ namespace graf {
 namespace {
 
 thread_local std::string t_last_error;
+thread_local int t_launches = 0;   // kernels / memsets enqueued by this thread's last entry-point call
 thread_local cudaEvent_t t_prof_start = nullptr, t_prof_stop = nullptr;
 
 cudaError_t prof_mark(bool start, cudaStream_t st) {
   cudaEvent_t ev = start ? t_prof_start : t_prof_stop;
   if (!t_prof_start || !t_prof_stop) return cudaSuccess;
+  // inside stream capture the record must be an external event node to be timeable
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    return cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
   return cudaEventRecord(ev, st);
 }
 
@@ -378,6 +383,7 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    ++t_launches;
   }
   return cudaSuccess;
 }
@@ -473,7 +479,9 @@ cudaError_t prepare_spad(const Plan& pl, const graf_af_desc* af, const void* s, 
   const long long total = af->batch * (long long)(af->n + af->m);
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
   pad_s_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(s), sp, af->n, af->m, af->batch);
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) ++t_launches;
+  return e;
 }
 
 graf_status common_checks(const graf_af_desc* af, const graf_loss_desc* L, const void* s, void* surface,
@@ -540,6 +548,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
     finalize_kernel<<<(unsigned)nb, 256, 0, st>>>(fc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "finalize_kernel launch");
+    ++t_launches;
   }
   return GRAF_OK;
 }
@@ -555,6 +564,7 @@ graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L,
   r.out = out;
   partials_reduce_kernel<<<(r.B + 127) / 128, 128, 0, st>>>(r);
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) ++t_launches;
   return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "partials_reduce_kernel launch");
 }
 
@@ -581,6 +591,8 @@ const char* graf_status_string(graf_status s) {
 
 const char* graf_last_error(void) { return t_last_error.c_str(); }
 
+int32_t graf_last_launch_count(void) { return t_launches; }
+
 size_t graf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) {
   if (check_af(af) != GRAF_OK) return 0;
   if (loss && check_loss(af, loss) != GRAF_OK) return 0;
@@ -592,6 +604,7 @@ size_t graf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) 
 
 graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s, void* surface,
                             graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
+  t_launches = 0;
   graf_status st = common_checks(af, loss, s, surface, false);
   if (st) return st;
   if (loss && !partials) return fail(GRAF_EINVAL, "loss given but partials is NULL");
@@ -625,6 +638,7 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
 graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
                               const graf_partials* global, double* loss_out, void* grad, void* surface, void* ws,
                               size_t ws_bytes, void* stream) {
+  t_launches = 0;
   graf_status st = common_checks(af, loss, s, surface, false);
   if (st) return st;
   if (!loss) return fail(GRAF_EINVAL, "loss descriptor is NULL");
@@ -639,6 +653,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   if (pl.U == 0) {
     e = cudaMemsetAsync(grad, 0, sizeof(float2) * (size_t)af->batch * af->n, cs);
     if (e != cudaSuccess) return cuda_fail(e, "zero grad");
+    ++t_launches;
     if (loss_out && !global) return fail(GRAF_EINVAL, "shard with no rows cannot compute the loss without `global`");
     // loss from global partials via the finalize path with P partial records absent
   }
@@ -692,6 +707,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
 
 graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
                              size_t ws_bytes, void* stream) {
+  t_launches = 0;
   graf_status st = common_checks(af, nullptr, s, nullptr, true);
   if (st) return st;
   if (!dA || !aligned8(dA)) return fail(GRAF_EINVAL, "dA is NULL or not 8-byte aligned");
@@ -720,6 +736,7 @@ graf_status graf_set_profile_events(void* start, void* stop) {
 
 graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partials* shards, int32_t G, int64_t B,
                                   graf_partials* out, int32_t on_device, void* stream) {
+  t_launches = 0;
   if (!loss || !shards || !out) return fail(GRAF_EINVAL, "NULL argument");
   if (G < 1 || B < 1) return fail(GRAF_EINVAL, "G = %d, B = %lld", G, (long long)B);
   const float T = loss->lambda_psl != 0.f ? loss->temperature : 1.f;
@@ -728,6 +745,7 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
     CombineParams c{shards, G, (int)B, T, out};
     combine_partials_kernel<<<(unsigned)((B + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(c);
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) ++t_launches;
     return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "combine_partials_kernel launch");
   }
   for (int64_t b = 0; b < B; ++b) {

@@ -19,4 +19,9 @@ if [ -n "$NCU" ]; then
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:af_rows_kernel -s 2 -c 1 \
      -o gpurun_out/prof_${TAG}_c$CFG python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --settle-s 0 > gpurun_out/ncu_full_$TAG.log 2>&1
   echo "ncu full exit=$?"
+  python scripts/ncu_summary.py gpurun_out/prof_${TAG}_c$CFG.ncu-rep gpurun_out/sum_${TAG}_c$CFG.txt > /dev/null 2>&1
+  python scripts/ncu_mix.py gpurun_out/prof_${TAG}_c$CFG.ncu-rep > gpurun_out/mix_${TAG}_c$CFG.txt 2>&1
+  ncu -i gpurun_out/prof_${TAG}_c$CFG.ncu-rep --page source --csv --print-source cuda > gpurun_out/src_${TAG}_c$CFG.csv 2>/dev/null
+  SZ=$(stat -c %s gpurun_out/prof_${TAG}_c$CFG.ncu-rep 2>/dev/null || echo 0)
+  if [ "$SZ" -gt 25000000 ]; then rm -f gpurun_out/prof_${TAG}_c$CFG.ncu-rep; fi
 fi
