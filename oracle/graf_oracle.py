@@ -59,8 +59,14 @@ __all__ = [
 # ---------------------------------------------------------------------------
 # index conventions
 # ---------------------------------------------------------------------------
-def delay_rows(n: int, k_max: Optional[int] = None) -> np.ndarray:
-    """Delays k = -K..K with K = min(k_max, N-1) (north star: k in +-(N-1))."""
+def delay_rows(n: int, k_max: Optional[int] = None, periodic: bool = False) -> np.ndarray:
+    """Delays k = -K..K with K = min(k_max, N-1) (north star: k in +-(N-1)).
+    periodic (the paper's circular Eq. 2): the distinct residues k mod N
+    with circular distance <= k_max, as k in (-N/2, N/2] (K = min(k_max, N//2))."""
+    if periodic:
+        K = n // 2 if k_max is None else min(k_max, n // 2)
+        lo = -K + 1 if 2 * K == n else -K
+        return np.arange(lo, K + 1)
     K = n - 1 if k_max is None else min(k_max, n - 1)
     return np.arange(-K, K + 1)
 
@@ -97,11 +103,16 @@ def dft_matrix(n: int, M: int, bins: np.ndarray, sign: int = -1) -> np.ndarray:
     return np.exp(sign * 2j * np.pi * ph / M)
 
 
-def lag_products(s: np.ndarray, rows: np.ndarray) -> np.ndarray:
+def lag_products(s: np.ndarray, rows: np.ndarray, periodic: bool = False) -> np.ndarray:
     """R[i, n] = s[n]*conj(s[n-k_i]) when 0 <= n-k_i < N, else 0 (Eqs. 8-10,
-    aperiodic reading R1).  rows: integer delays k."""
+    aperiodic reading R1).  rows: integer delays k.
+    periodic: R[i, n] = s[n]*conj(s[(n-k_i) mod N]) for every n (Eqs. 8-10 exactly as
+    printed: the circulant shift matrix S[k,n] = s[(n-k) mod N])."""
     s = np.asarray(s, dtype=np.complex128)
     n = s.shape[0]
+    if periodic:
+        return np.stack([s * np.conj(s[(np.arange(n) - int(k)) % n]) for k in rows]) if len(rows) else \
+            np.zeros((0, n), dtype=np.complex128)
     R = np.zeros((len(rows), n), dtype=np.complex128)
     for i, k in enumerate(rows):
         k = int(k)
@@ -112,27 +123,32 @@ def lag_products(s: np.ndarray, rows: np.ndarray) -> np.ndarray:
 
 
 def ambiguity(s: np.ndarray, M: int, rows: Optional[np.ndarray] = None,
-              bins: Optional[np.ndarray] = None) -> np.ndarray:
-    """A[rows, bins] (complex128), direct O(N*|rows|*|bins|) evaluation."""
+              bins: Optional[np.ndarray] = None, periodic: bool = False) -> np.ndarray:
+    """A[rows, bins] (complex128), direct O(N*|rows|*|bins|) evaluation.
+    periodic: the circular lag products (the paper's Eq. 2 with the FFT's e^{-j},
+    reading R2; M = N in the paper)."""
     s = np.asarray(s, dtype=np.complex128)
     n = s.shape[0]
-    rows = delay_rows(n) if rows is None else np.asarray(rows)
+    rows = delay_rows(n, periodic=periodic) if rows is None else np.asarray(rows)
     bins = np.arange(M) if bins is None else np.asarray(bins)
-    return lag_products(s, rows) @ dft_matrix(n, M, bins)
+    return lag_products(s, rows, periodic) @ dft_matrix(n, M, bins)
 
 
 def surface(s: np.ndarray, M: int, kind: str = "c64", layout: str = "centered",
             normalize_output: bool = False, k_begin: Optional[int] = None,
-            k_end: Optional[int] = None) -> np.ndarray:
+            k_end: Optional[int] = None, periodic: bool = False) -> np.ndarray:
     """The forward-surface output the ABI writes: rows k_begin..k_end-1 (row
     index k - k_begin), Doppler raw m or centred j = d + M/2 (Alg. 1 step 5,
     P:L252).  kind: 'c64' -> A, 'abs' -> |A|, 'pow' -> |A|^2 (Alg. 1 step 4,
     P:L251).  normalize_output divides A by E (Eq. 17 analogue: max chi = E^2,
     P:L265-268, reading R6)."""
     n = len(s)
-    kb = -(n - 1) if k_begin is None else k_begin
+    if periodic:   # Alg. 1 (P:L239-256): rows k = 0..N-1, or any window of <= N delays
+        kb = 0 if k_begin is None else k_begin
+    else:
+        kb = -(n - 1) if k_begin is None else k_begin
     ke = n if k_end is None else k_end
-    A = ambiguity(s, M, rows=np.arange(kb, ke))
+    A = ambiguity(s, M, rows=np.arange(kb, ke), periodic=periodic)
     if normalize_output:
         A = A / energy(s)
     if layout == "centered":
@@ -170,9 +186,10 @@ class LossSpec:
         return cls(**{k: v for k, v in d.items() if k in cls.__dataclass_fields__})
 
 
-def region(n: int, M: int, spec: LossSpec):
-    """rows (k), bins (m), mask [rows, bins] (bool), weights [rows, bins]."""
-    rows = delay_rows(n, spec.k_max)
+def region(n: int, M: int, spec: LossSpec, periodic: bool = False):
+    """rows (k), bins (m), mask [rows, bins] (bool), weights [rows, bins].
+    periodic: rows are the residues with circular delay distance <= k_max."""
+    rows = delay_rows(n, spec.k_max, periodic)
     bins = centred_bins(M, spec.d_max)
     d = centred(bins, M)
     mainlobe = (np.abs(rows)[:, None] <= spec.ml_k) & (np.abs(d)[None, :] <= spec.ml_d)
@@ -183,15 +200,15 @@ def region(n: int, M: int, spec: LossSpec):
     return rows, bins, mask, w
 
 
-def loss_terms(s: np.ndarray, M: int, spec: LossSpec) -> dict:
+def loss_terms(s: np.ndarray, M: int, spec: LossSpec, periodic: bool = False) -> dict:
     """All step 3-5 quantities for one waveform (dict of numpy values)."""
     s = np.asarray(s, dtype=np.complex128)
     n = s.shape[0]
-    rows, bins, mask, w = region(n, M, spec)
+    rows, bins, mask, w = region(n, M, spec, periodic)
     if not mask.any():
         raise ValueError("empty sidelobe region (S:L302)")
     E = energy(s)
-    A = ambiguity(s, M, rows, bins)
+    A = ambiguity(s, M, rows, bins, periodic)
     chi = A.real ** 2 + A.imag ** 2
     x = chi / E ** 2 if spec.normalize else chi
     S = float(np.sum(w[mask] * chi[mask]))
@@ -206,20 +223,28 @@ def loss_terms(s: np.ndarray, M: int, spec: LossSpec) -> dict:
                 S=S, isl=isl, c=c, Z=Z, lse=lse, loss=L, count=int(mask.sum()))
 
 
-def loss(s: np.ndarray, M: int, spec: LossSpec) -> float:
-    return loss_terms(s, M, spec)["loss"]
+def loss(s: np.ndarray, M: int, spec: LossSpec, periodic: bool = False) -> float:
+    return loss_terms(s, M, spec, periodic)["loss"]
 
 
 # ---------------------------------------------------------------------------
 # Steps 6-8: the Wirtinger adjoint
 # ---------------------------------------------------------------------------
-def correlate(s: np.ndarray, H: np.ndarray, rows: np.ndarray) -> np.ndarray:
+def correlate(s: np.ndarray, H: np.ndarray, rows: np.ndarray, periodic: bool = False) -> np.ndarray:
     """Step 8 without the normalization term:
     g[p] = sum_k H[k,p]*s[p-k] + sum_k conj(H[k,p+k])*s[p+k], valid indices only
-    (adjoint of R[k,n] = s[n]*conj(s[n-k]) w.r.t. s*, Eq. 15)."""
+    (adjoint of R[k,n] = s[n]*conj(s[n-k]) w.r.t. s*, Eq. 15).
+    periodic: every index taken mod N (adjoint of the circulant lag products)."""
     s = np.asarray(s, dtype=np.complex128)
     n = s.shape[0]
     g = np.zeros(n, dtype=np.complex128)
+    if periodic:
+        idx = np.arange(n)
+        for i, k in enumerate(rows):
+            k = int(k)
+            g += H[i] * s[(idx - k) % n]                      # term 1: p = n
+            np.add.at(g, (idx - k) % n, np.conj(H[i]) * s)    # term 2: p = (n - k) mod N
+        return g
     for i, k in enumerate(rows):
         k = int(k)
         lo, hi = max(0, k), min(n, n + k)      # valid n (= p for term 1)
@@ -233,7 +258,7 @@ def correlate(s: np.ndarray, H: np.ndarray, rows: np.ndarray) -> np.ndarray:
 
 
 def adjoint(s: np.ndarray, M: int, G: np.ndarray, rows: np.ndarray,
-            bins: Optional[np.ndarray] = None) -> np.ndarray:
+            bins: Optional[np.ndarray] = None, periodic: bool = False) -> np.ndarray:
     """Generic backward (graf_af_backward): given G = dL/dA* on rows x bins,
     return dL/ds* = steps 7-8 (no normalization term: A itself does not
     depend on E)."""
@@ -241,19 +266,19 @@ def adjoint(s: np.ndarray, M: int, G: np.ndarray, rows: np.ndarray,
     n = s.shape[0]
     bins = np.arange(M) if bins is None else np.asarray(bins)
     H = np.asarray(G, dtype=np.complex128) @ dft_matrix(n, M, bins, sign=+1).T
-    return correlate(s, H, rows)
+    return correlate(s, H, rows, periodic)
 
 
-def loss_and_grad(s: np.ndarray, M: int, spec: LossSpec):
+def loss_and_grad(s: np.ndarray, M: int, spec: LossSpec, periodic: bool = False):
     """(L, g = dL/ds*, terms) for one waveform."""
-    t = loss_terms(s, M, spec)
+    t = loss_terms(s, M, spec, periodic)
     s = np.asarray(s, dtype=np.complex128)
     E, A, chi, x, mask, w = t["E"], t["A"], t["chi"], t["x"], t["mask"], t["w"]
     T = spec.temperature
     fp = np.zeros_like(chi)
     fp[mask] = spec.lambda_isl * w[mask] + spec.lambda_psl * np.exp((x[mask] - t["lse"]) / T)
     G = fp * A / E ** 2 if spec.normalize else fp * A
-    g = adjoint(s, M, G, t["rows"], t["bins"])
+    g = adjoint(s, M, G, t["rows"], t["bins"], periodic)
     if spec.normalize:
         g = g - (2.0 / E ** 3) * float(np.sum(fp[mask] * chi[mask])) * s
     t["fprime"] = fp

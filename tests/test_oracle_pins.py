@@ -347,3 +347,86 @@ def test_chunked_equals_one_shot():
     L2, g2, t2 = O.loss_and_grad_chunked(s, M, spec, chunk_rows=7, chunk_bins=13)
     assert abs(L1 - L2) < 1e-12 * abs(L1)
     np.testing.assert_allclose(g1, g2, atol=1e-13 * max(1, np.abs(g1).max()) + 1e-15)
+
+
+# ---------------------------------------------------------------- periodic (the paper's Alg. 1)
+# The circular surface of Eq. 2 / Alg. 1, pinned to the
+# independent aperiodic path (fold identity), to Eq. 2 as printed (mirrored
+# Doppler, reading R2), and by the periodic closed forms / invariants.
+PSPECS = [
+    dict(k_max=2, d_max=3, ml_k=0, ml_d=0, lambda_isl=1.0, lambda_psl=0.0, normalize=1),
+    dict(k_max=4, d_max=4, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05, normalize=1),
+    dict(k_max=3, d_max=2, ml_k=1, ml_d=0, lambda_isl=0.5, lambda_psl=0.0, normalize=0),
+]
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_periodic_surface_is_fold_and_mirrored_eq2(n):
+    s = rs(n, 60)
+    rows, A = full(s, n)
+    P = O.ambiguity(s, n, rows=np.arange(n), periodic=True)
+    X = O.periodic_ambiguity(s)
+    m = np.arange(n)
+    for k in range(n):
+        fold = A[row(rows, k)] + (A[row(rows, k - n)] if k > 0 else 0)
+        np.testing.assert_allclose(P[k], fold, atol=1e-12 * O.energy(s))
+        np.testing.assert_allclose(P[k], X[k, (-m) % n], atol=1e-12 * O.energy(s))
+    # negative delays are the residues: row -k == row N-k
+    Pn = O.ambiguity(s, n, rows=np.arange(-(n - 1), 0), periodic=True)
+    np.testing.assert_allclose(Pn, P[1:], atol=1e-12 * O.energy(s))
+    # volume: sum |A_per|^2 = N E^2
+    assert abs(np.sum(np.abs(P) ** 2) - n * O.energy(s) ** 2) < 1e-10 * n * O.energy(s) ** 2
+
+
+@pytest.mark.parametrize("code", ["frank", "p4"])
+def test_periodic_perfect_acf(code):
+    n = 64
+    s = (frank(n) if code == "frank" else p4(n)).astype(complex)
+    P = O.ambiguity(s, n, rows=np.arange(n), bins=np.array([0]), periodic=True)
+    assert abs(P[0, 0] - n) < 1e-5 and np.abs(P[1:, 0]).max() < 1e-5
+
+
+@pytest.mark.parametrize("n", [8, 9, 16])
+def test_periodic_full_plane_closed_forms(n):
+    s = rs(n, 61)
+    E = O.energy(s)
+    spec = O.LossSpec(k_max=n, d_max=n, lambda_isl=1.0, normalize=1)
+    L, g, t = O.loss_and_grad(s, n, spec, periodic=True)
+    assert t["count"] == n * n - 1
+    assert abs(L - (n - 1)) < 1e-10 * n and np.abs(g).max() < 1e-11 * n
+    spec.normalize = 0
+    L, g, _ = O.loss_and_grad(s, n, spec, periodic=True)
+    assert abs(L - (n - 1) * E ** 2) < 1e-11 * n * E ** 2
+    np.testing.assert_allclose(g, 2 * (n - 1) * E * s, atol=1e-10 * n * E)
+
+
+@pytest.mark.parametrize("si", range(len(PSPECS)))
+@pytest.mark.parametrize("n", [8, 9])
+def test_periodic_gradient_central_differences(si, n):
+    s = rs(n, 70 + si)
+    spec = O.LossSpec(**PSPECS[si])
+    L, g, _ = O.loss_and_grad(s, n, spec, periodic=True)
+    eps = 1e-6
+    fd = np.zeros(n, complex)
+    for p in range(n):
+        for unit in (1.0, 1j):
+            sp = s.copy(); sp[p] += eps * unit
+            sm = s.copy(); sm[p] -= eps * unit
+            d = (O.loss(sp, n, spec, periodic=True) - O.loss(sm, n, spec, periodic=True)) / (2 * eps)
+            fd[p] += d * (1.0 if unit == 1.0 else 1j)
+    np.testing.assert_allclose(2 * g, fd, atol=1e-7 * max(1.0, np.abs(fd).max()))
+    sc = max(1.0, np.abs(g).max() * np.abs(s).max() * n)
+    assert abs(np.vdot(g, s).imag) < 1e-11 * sc
+    if spec.normalize:
+        assert abs(np.vdot(g, s).real) < 1e-11 * sc
+
+
+def test_periodic_adjoint_inner_product_identity():
+    n = 12
+    s, dlt = rs(n, 80), rs(n, 81)
+    rows = np.arange(-5, 7)
+    G = rs(len(rows) * n, 82).reshape(len(rows), n)
+    lin = (O.ambiguity(s + dlt, n, rows, periodic=True) - O.ambiguity(s - dlt, n, rows, periodic=True)) / 2
+    lhs = np.vdot(G, lin).real
+    rhs = np.vdot(O.adjoint(s, n, G, rows, periodic=True), dlt).real
+    assert abs(lhs - rhs) < 1e-11 * max(1, abs(lhs))
