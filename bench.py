@@ -145,9 +145,11 @@ def cpu_baseline(w: dict, budget_s: float = 12.0) -> dict:
             s_small = s
             O.loss_and_grad_chunked(s_small, M, spec)
         else:
-            O.loss_and_grad(s, M, spec)
+            per = w.get("periodic", False)
+            O.loss_and_grad(s, M, spec, periodic=per)
             if w["cfg"]["surface"]:
-                O.surface(s, M, w["cfg"]["surface"], "centered")
+                O.surface(s, M, w["cfg"]["surface"], "centered", periodic=per,
+                          **(dict(k_begin=-(N // 2), k_end=N // 2) if per else {}))
         done += 1
         b += 1
         el = time.perf_counter() - t0
@@ -173,9 +175,11 @@ def run_reference(args, w) -> None:
     def step(i):
         for j in range(per_step):
             s = config_waveforms(w["cid"], batch=1, start=(i * per_step + j) % w["B"])[0]
-            O.loss_and_grad(s, w["M"], spec)
+            per = w.get("periodic", False)
+            O.loss_and_grad(s, w["M"], spec, periodic=per)
             if w["cfg"]["surface"]:
-                O.surface(s, w["M"], w["cfg"]["surface"], "centered")
+                O.surface(s, w["M"], w["cfg"]["surface"], "centered", periodic=per,
+                          **(dict(k_begin=-(w["N"] // 2), k_end=w["N"] // 2) if per else {}))
 
     for i in range(args.warmup):
         step(i)
@@ -212,13 +216,25 @@ def main():
     ap.add_argument("--settle-s", type=float, default=1.0)
     ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward"],
                     help="forward: full-surface mode (graf_af_forward writes the config's surface, no loss)")
+    ap.add_argument("--periodic", action="store_true",
+                    help="the paper's circular surface (Eq. 2 / Alg. 1, SURVEY 8(f) NEXT-1); needs M == N")
     args = ap.parse_args()
     w = workload(args.config)
+    w["periodic"] = bool(args.periodic)
+    if args.periodic:
+        if w["N"] != w["M"]:
+            raise SystemExit("--periodic needs a config with M == N (c1, c2, c3, c5)")
+        # folded circular rows k = 0..min(k_max, N/2), same FFT work per row
+        w["rows"] = min(w["loss"]["k_max"], w["N"] // 2) + 1
+        w["flops"] = w["B"] * w["rows"] * w["ffts"] * 5.0 * w["M"] * math.log2(w["M"])
+        if w["cfg"]["surface"]:
+            w["surf_bytes"] = w["B"] * w["N"] * w["M"] * (8 if w["cfg"]["surface"] == "c64" else 4)
+        w["note"] = (w["note"] + "; " if w["note"] else "") + "periodic (circular) surface, paper Eq. 2 / Alg. 1"
     if args.mode == "forward":
         if not w["cfg"]["surface"]:
             raise SystemExit("--mode forward needs a config with a surface (c1, c3)")
         # folded rows covering the whole surface window, one forward FFT each
-        w["flops"] = w["B"] * w["N"] * 5.0 * w["M"] * math.log2(w["M"])
+        w["flops"] = w["B"] * (w["N"] // 2 + 1 if args.periodic else w["N"]) * 5.0 * w["M"] * math.log2(w["M"])
         w["io_bytes"] = w["B"] * w["N"] * 8
         w["launches"] = 1
         w["note"] = "full-surface mode: graf_af_forward writes the surface; no loss or gradient"
@@ -249,8 +265,11 @@ def main():
     grad = torch.empty((B, N), dtype=torch.complex64, device=dev)
     loss_out = torch.empty((B,), dtype=torch.float64, device=dev)
     surf = None
+    # periodic: Alg. 1's N x N surface with both axes fftshifted (delays [-N/2, N/2))
+    kb = dict(periodic=True, k_begin=-(N // 2), k_end=N // 2) if args.periodic else {}
     if out:
-        surf = torch.empty((B, 2 * N - 1, M), dtype=torch.complex64 if out == "c64" else torch.float32, device=dev)
+        nrows = N if args.periodic else 2 * N - 1
+        surf = torch.empty((B, nrows, M), dtype=torch.complex64 if out == "c64" else torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
     ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -266,10 +285,10 @@ def main():
             sharding.delay_sharded_loss_grad(s, M, spec, backend=tb)
             return
         if args.mode == "forward":
-            graf.af_forward(s, M, out=out, layout="centered", ws=ws, surface=surf, stream=st)
+            graf.af_forward(s, M, out=out, layout="centered", ws=ws, surface=surf, stream=st, **kb)
             return
         graf.af_loss_grad(s, M, spec, out=out, layout="centered", ws=ws, grad=grad, loss_out=loss_out,
-                          surface=surf, stream=st)
+                          surface=surf, stream=st, **kb)
 
     with torch.cuda.stream(stream):
         call(stream)                                    # twiddle init + workspace, before capture
@@ -370,8 +389,9 @@ def main():
             if delay:
                 lo, gr = sharding.delay_sharded_loss_grad(s_dev2, M, spec)
             elif args.mode == "forward":
-                sf, _ = graf.af_forward(s_dev2, M, out=out, layout="centered", ws=ws, surface=surf, stream=stream)
-                zrow = sf[:, N - 1, :]                    # zero-delay cut of every surface
+                sf, _ = graf.af_forward(s_dev2, M, out=out, layout="centered", ws=ws, surface=surf, stream=stream,
+                                        **kb)
+                zrow = sf[:, N // 2 if args.periodic else N - 1, :]   # zero-delay cut of every surface
                 if zrow_host is None:
                     zrow_host = torch.empty(zrow.shape, dtype=zrow.dtype).pin_memory()
                 zrow_host.copy_(zrow, non_blocking=True)
@@ -382,7 +402,7 @@ def main():
                 continue
             else:
                 lo, gr, _ = graf.af_loss_grad(s_dev2, M, spec, out=out, layout="centered", ws=ws, surface=surf,
-                                              stream=stream)
+                                              stream=stream, **kb)
             l_host.copy_(lo, non_blocking=True)
             g_host.copy_(gr, non_blocking=True)
             b_.record(stream)

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GRAF_ABI_VERSION 1
+#define GRAF_ABI_VERSION 2
 #define GRAF_MAX_M 16384
 
 typedef enum {
@@ -81,6 +81,14 @@ typedef struct {
   int32_t normalize_output; /* 1: surface holds A/E, |A|/E, chi/E^2 (Eq. 17 analogue: max chi = E^2, L265-268) */
   int32_t shard_index;      /* delay sharding of the LOSS rows: this call handles the folded */
   int32_t shard_count;      /*   delay rows k >= 0 with k % shard_count == shard_index (0/1 = all) */
+  int32_t periodic;         /* 0: aperiodic (above).  1: the paper's circular surface, Eq. 2 (L121)
+                               and Algorithm 1 (L239-256) with the FFT's e^{-j} (reading R2):
+                               A[k,m] = sum_{n<N} s[n] conj(s[(n-k) mod N]) exp(-2 pi j m n/M);
+                               requires M == N.  Rows of the window are delays taken mod N
+                               (k_end - k_begin <= N; [-N/2, N/2) with GRAF_DOPPLER_CENTERED is
+                               Alg. 1's two-axis fftshift, L252).  The loss region uses the
+                               circular delay distance min(k mod N, N - k mod N) <= k_max and
+                               weights w_k[k + N - 1] for k in (-N/2, N/2].  (ABI v2) */
 } graf_af_desc;
 
 /* Loss over the sidelobe region Omega_s (never defined by the paper,

@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # GRAF_LIB_PATH: tuning builds only (scripts/tune.py); the default is the in-tree library.
 LIB_PATH = os.environ.get("GRAF_LIB_PATH") or os.path.join(PKG, "libgraf.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_ENONFINITE, GRAF_EWORKSPACE = range(6)
 OUT_NONE, OUT_C64, OUT_ABS_F32, OUT_POW_F32 = range(4)
 DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
@@ -24,7 +24,7 @@ class AfDesc(ctypes.Structure):
     _fields_ = [("abi_version", c_int32), ("n", c_int32), ("m", c_int32), ("out_kind", c_int32),
                 ("batch", c_int64), ("k_begin", c_int32), ("k_end", c_int32),
                 ("doppler_layout", c_int32), ("normalize_output", c_int32),
-                ("shard_index", c_int32), ("shard_count", c_int32)]
+                ("shard_index", c_int32), ("shard_count", c_int32), ("periodic", c_int32)]
 
 
 class LossDesc(ctypes.Structure):

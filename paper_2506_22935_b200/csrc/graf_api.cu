@@ -146,6 +146,9 @@ graf_status check_af(const graf_af_desc* af) {
   const int sc = af->shard_count <= 0 ? 1 : af->shard_count;
   if (af->shard_index < 0 || af->shard_index >= sc)
     return fail(GRAF_EINVAL, "shard_index %d not in [0, %d)", af->shard_index, sc);
+  if (af->periodic != 0 && af->periodic != 1) return fail(GRAF_EINVAL, "periodic must be 0 or 1");
+  if (af->periodic && af->m != af->n)
+    return fail(GRAF_EUNSUPPORTED, "periodic surface needs M == N (M = %d, N = %d)", af->m, af->n);
   return GRAF_OK;
 }
 
@@ -153,6 +156,9 @@ graf_status check_window(const graf_af_desc* af) {
   if (af->k_begin < -(af->n - 1) || af->k_end > af->n || af->k_begin >= af->k_end)
     return fail(GRAF_EINVAL, "row window [%d, %d) not inside [-(N-1), N) = [%d, %d)", af->k_begin, af->k_end,
                 -(af->n - 1), af->n);
+  if (af->periodic && af->k_end - af->k_begin > af->n)
+    return fail(GRAF_EINVAL, "periodic row window [%d, %d) holds more than N = %d delays", af->k_begin,
+                af->k_end, af->n);
   return GRAF_OK;
 }
 
@@ -163,7 +169,7 @@ graf_status check_loss(const graf_af_desc* af, const graf_loss_desc* L) {
   if (L->lambda_psl != 0.f && !(L->temperature > 0.f)) return fail(GRAF_EINVAL, "temperature must be > 0");
   if (!std::isfinite(L->lambda_isl) || !std::isfinite(L->lambda_psl))
     return fail(GRAF_EINVAL, "non-finite lambda");
-  const int kl = std::min(L->k_max, af->n - 1);
+  const int kl = std::min(L->k_max, af->periodic ? af->n / 2 : af->n - 1);
   const int dl = std::min(L->d_max, af->m / 2);
   const bool nonempty = kl > L->ml_k || dl > L->ml_d;
   if (!nonempty) return fail(GRAF_EINVAL, "empty sidelobe region (mainlobe covers the mask)");
@@ -208,10 +214,16 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
     pl.U = af->k_end - af->k_begin;
   } else {
     const bool surf = af->out_kind != GRAF_OUT_NONE;
-    const int kloss = L ? std::min(L->k_max, N - 1) : -1;
+    const int kfold = af->periodic ? N / 2 : N - 1;   // largest folded delay
+    const int kloss = L ? std::min(L->k_max, kfold) : -1;
     if (surf) {
       int lo, hi;
-      folded_window(af->k_begin, af->k_end, &lo, &hi);
+      if (af->periodic) {   // every folded residue pair may meet the window
+        lo = 0;
+        hi = kfold;
+      } else {
+        folded_window(af->k_begin, af->k_end, &lo, &hi);
+      }
       if (L) {
         lo = 0;
         hi = std::max(hi, kloss);
@@ -229,7 +241,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   }
   pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? (size_t)ci.S * N : 0) + (size_t)ci.tab1);
-  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512) {
+  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512 && !af->periodic) {
     pl.gpad_ok = true;
     pl.smem_gpad = sizeof(float2) * (size_t)ci.S * N;
   }
@@ -429,7 +441,7 @@ cudaError_t launch_rows(Plan& pl, const RowParams& rp, int B, cudaStream_t st, i
 void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
   const int N = af->n, M = af->m;
   rp.loss_on = 1;
-  rp.kloss = std::min(L->k_max, N - 1);
+  rp.kloss = std::min(L->k_max, af->periodic ? N / 2 : N - 1);
   rp.d_max = L->d_max;
   rp.ml_k = L->ml_k;
   rp.ml_d = L->ml_d;
@@ -441,9 +453,9 @@ void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
   rp.invT = 1.f / rp.T;
   rp.normalize = L->normalize;
   // reading R13: constant-sum region -> centred soft-PSL weights
-  const bool full = rp.kloss == N - 1 && L->d_max >= M / 2 && L->ml_k == 0 && L->ml_d == 0;
+  const bool full = rp.kloss == (af->periodic ? N / 2 : N - 1) && L->d_max >= M / 2 && L->ml_k == 0 && L->ml_d == 0;
   rp.centred = (L->normalize && !L->w_k && !L->w_d && full && L->lambda_psl != 0.f) ? 1 : 0;
-  rp.omega = (double)(2 * N - 1) * M - 1.0;
+  rp.omega = (double)(af->periodic ? N : 2 * N - 1) * M - 1.0;   // |Omega| of the full plane
   rp.xbar = (float)((M - 1) / rp.omega);
 }
 
@@ -463,6 +475,7 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
   rp.norm_out = af->normalize_output;
   rp.shard_index = af->shard_index;
   rp.shard_count = af->shard_count <= 0 ? 1 : af->shard_count;
+  rp.periodic = af->periodic;
   rp.T = 1.f;
   rp.invT = 1.f;
   char* w = static_cast<char*>(ws);
@@ -478,7 +491,7 @@ cudaError_t prepare_spad(const Plan& pl, const graf_af_desc* af, const void* s, 
   float2* sp = reinterpret_cast<float2*>(static_cast<char*>(ws) + pl.off_spad);
   const long long total = af->batch * (long long)(af->n + af->m);
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-  pad_s_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(s), sp, af->n, af->m, af->batch);
+  pad_s_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(s), sp, af->n, af->m, af->batch, af->periodic);
   const cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++t_launches;
   return e;

@@ -60,6 +60,7 @@ struct RowParams {
                        // buffer (stg_floats per slot), 2 aliased to the slot's exchange buffer
   int stg_floats;      // staging floats per row slot (2*M*{1,2}: rows +k and -k)
   int gpad;            // 1: left-padded gradient accumulators (M == N, folded rows)
+  int periodic;        // 1: circular lag products (the paper's Eq. 2 / Alg. 1), M == N
   // fused finalize (K_ISL, P <= 8 CTAs per waveform launched as one thread-block
   // cluster): cluster rank 0 combines the CTAs' partials over distributed shared
   // memory and writes loss and grad directly (no partial records, no finalize kernel)
@@ -423,7 +424,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // ---- a0: stage s, zero the gradient accumulators, energy
   if constexpr (C::S_SMEM) {
     for (int i = threadIdx.x; i < N + M; i += THREADS)
-      s_pad[i] = (i >= N && i < 2 * N) ? sg[i - N] : make_float2(0.f, 0.f);
+      // aperiodic: N zeros on the left; periodic: a copy of s, so s_pad[n - k] = s[(n - k) mod N]
+      s_pad[i] = (i < 2 * N && (i >= N || p.periodic)) ? sg[i >= N ? i - N : i] : make_float2(0.f, 0.f);
   }
   if constexpr (GRAD) {
     if constexpr (C::G_SMEM) {
@@ -505,8 +507,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     const int u = it * rows_per_iter + pb * S + slot;
     const bool valid = u < p.U;
     const int k = p.row_lo + (valid ? u : 0) * p.row_step;
-    const int lo = k > 0 ? k : 0;
-    const int hi = k < 0 ? N + k : N;
+    // time support of the row (periodic rows use every n < N = M)
+    const int lo = (k > 0 && !p.periodic) ? k : 0;
+    const int hi = (k < 0 && !p.periodic) ? N + k : N;
     // slots e whose time index n lies in the row's support [lo, hi)
     VMask vmask;
     if constexpr (!SPLIT) {
@@ -526,10 +529,19 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     if constexpr (KIND != K_ADJ) {
       // ---- a1: lag product into the first-pass registers (time index n = t + e*T);
       //      s_pad makes out-of-support terms exactly zero
-      const bool wpos = valid && p.surface && k >= p.kb && k < p.ke;
-      const bool wneg = valid && p.surface && k > 0 && -k >= p.kb && -k < p.ke;
+      // window rows of delays +k and -k (periodic: the window row holding that residue mod N)
+      const int nrow = p.ke - p.kb;
+      auto wrow = [&](int kk) {
+        int q = kk - p.kb;
+        if (p.periodic && (q < 0 || q >= nrow)) q += (q < 0 ? N : -N);
+        return (q >= 0 && q < nrow) ? q : -1;
+      };
+      const bool self = (k == 0) || (p.periodic && 2 * k == N);   // row -k is row +k
+      const int rowp = wrow(k), rown = self ? -1 : wrow(-k);
+      const bool wpos = valid && p.surface && rowp >= 0;
+      const bool wneg = valid && p.surface && rown >= 0;
       lrow = valid && p.loss_on && k <= p.kloss && (k % p.shard_count) == p.shard_index;
-      const float mult = (k == 0) ? 1.f : 2.f;
+      const float mult = self ? 1.f : 2.f;
       if constexpr (!SPLIT) {
         const float2* a = sv + t;
         const float2* c = sv + t - k;
@@ -603,8 +615,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
                 bulk_store(dst, src, rb);
               }
             };
-            if (wpos) put(out + ((size_t)b * surf_rows + (k - p.kb)) * rb, sp);
-            if (wneg) put(out + ((size_t)b * surf_rows + (-k - p.kb)) * rb, sp + rb);
+            if (wpos) put(out + ((size_t)b * surf_rows + rowp) * rb, sp);
+            if (wneg) put(out + ((size_t)b * surf_rows + rown) * rb, sp + rb);
             bulk_commit();
           }
         }
@@ -613,8 +625,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         // column of frequency m in row +k: (m + lay) mod M; in row -k: (lay - m) mod M
         if (p.out_kind == GRAF_OUT_C64) {
           float2* out = reinterpret_cast<float2*>(p.surface);
-          float2* rp = out + ((size_t)b * surf_rows + (k - p.kb)) * M;
-          float2* rn = out + ((size_t)b * surf_rows + (-k - p.kb)) * M;
+          float2* rp = out + ((size_t)b * surf_rows + rowp) * M;
+          float2* rn = out + ((size_t)b * surf_rows + rown) * M;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int m = t + e * T;
@@ -627,8 +639,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
         } else {
           float* out = reinterpret_cast<float*>(p.surface);
-          float* rp = out + ((size_t)b * surf_rows + (k - p.kb)) * M;
-          float* rn = out + ((size_t)b * surf_rows + (-k - p.kb)) * M;
+          float* rp = out + ((size_t)b * surf_rows + rowp) * M;
+          float* rn = out + ((size_t)b * surf_rows + rown) * M;
           const bool absk = p.out_kind == GRAF_OUT_ABS_F32;
           const float sc = absk ? nrm : nrm * nrm;
 #pragma unroll
@@ -736,7 +748,26 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const int tb = SPLIT ? 2 * t : t;
         // predicated shared-memory read-modify-writes (no branches; an out-of-support
         // slot neither loads nor stores its accumulator)
-        if (KIND != K_ADJ && kGpadSizes && p.gpad) {
+        if (p.periodic) {
+          // circular lag products (M == N): every slot is in the support; term 1 reads
+          // s[(n - k) mod N] from the periodic copy in s_pad, term 2 wraps its position.
+          const int kc = k < 0 ? k + N : k;   // K_ADJ rows may be negative delays
+          {
+            float2* g1 = gacc + tb;
+            const float2* s1 = sv + tb - kc;
+#pragma unroll
+            for (int e = 0; e < E; ++e) g1[toff(e)] = cadd(g1[toff(e)], cmul(v[e], s1[toff(e)]));
+          }
+          sync();
+          {
+            const float2* s2 = sv + tb;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              float2* gq = gacc + ((tb + toff(e) - kc) & (N - 1));
+              *gq = cadd(*gq, cmulc(s2[toff(e)], v[e]));
+            }
+          }
+        } else if (KIND != K_ADJ && kGpadSizes && p.gpad) {
           // M == N, k >= 0: every term-1 position n < N is in the slot's range and
           // s[n - k] = 0 below the support; term-2 positions n - k >= -k land in the
           // left pad when n < k.  No predicates.
@@ -882,13 +913,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 
 // zero-padded copy of s for the global-memory path: s_pad[b][i] = s[b][i - N] for
 // i in [N, 2N), 0 elsewhere in [0, N + M)
-__global__ void pad_s_kernel(const float2* s, float2* s_pad, int N, int M, long long B) {
+__global__ void pad_s_kernel(const float2* s, float2* s_pad, int N, int M, long long B, int periodic) {
   const long long total = B * (long long)(N + M);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long b = i / (N + M);
     const int j = (int)(i - b * (N + M));
-    s_pad[i] = (j >= N && j < 2 * N) ? s[b * N + (j - N)] : make_float2(0.f, 0.f);
+    s_pad[i] = (j < 2 * N && (j >= N || periodic)) ? s[b * N + (j >= N ? j - N : j)] : make_float2(0.f, 0.f);
   }
 }
 

@@ -74,12 +74,15 @@ def _check_s(s: torch.Tensor) -> torch.Tensor:
 
 
 def _desc(s: torch.Tensor, M: int, out=None, layout="centered", k_begin=None, k_end=None,
-          normalize_output=False, shard=(0, 1)) -> L.AfDesc:
+          normalize_output=False, shard=(0, 1), periodic=False) -> L.AfDesc:
     B, N = s.shape
-    kb = -(N - 1) if k_begin is None else int(k_begin)
+    if periodic:   # Alg. 1: delays 0..N-1 (mod N)
+        kb = 0 if k_begin is None else int(k_begin)
+    else:
+        kb = -(N - 1) if k_begin is None else int(k_begin)
     ke = N if k_end is None else int(k_end)
     return L.AfDesc(L.ABI_VERSION, int(N), int(M), _OUT[out], int(B), kb, ke, _LAYOUT[layout],
-                    int(bool(normalize_output)), int(shard[0]), int(shard[1]))
+                    int(bool(normalize_output)), int(shard[0]), int(shard[1]), int(bool(periodic)))
 
 
 def workspace_bytes(desc: L.AfDesc, loss: Optional[L.LossDesc]) -> int:
@@ -112,10 +115,11 @@ def _surface_alloc(desc: L.AfDesc, device) -> Optional[torch.Tensor]:
 def af_forward(s: torch.Tensor, M: int, *, out: Optional[str] = "c64", layout: str = "centered",
                k_begin: Optional[int] = None, k_end: Optional[int] = None, normalize_output: bool = False,
                loss: Optional[LossSpec] = None, shard=(0, 1), ws: Optional[Workspace] = None,
-               surface: Optional[torch.Tensor] = None, stream=None):
-    """graf_af_forward: surface window and/or this shard's loss partials [B,4] (float64)."""
+               surface: Optional[torch.Tensor] = None, stream=None, periodic: bool = False):
+    """graf_af_forward: surface window and/or this shard's loss partials [B,4] (float64).
+    periodic=True: the paper's circular surface (Eq. 2 / Alg. 1), M == N."""
     s = _check_s(s)
-    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard)
+    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic)
     ld = loss.desc() if loss is not None else None
     if surface is None:
         surface = _surface_alloc(d, s.device)
@@ -132,10 +136,11 @@ def af_loss_grad(s: torch.Tensor, M: int, loss: LossSpec, *, global_partials: Op
                  out: Optional[str] = None, layout: str = "centered", k_begin=None, k_end=None,
                  normalize_output: bool = False, shard=(0, 1), ws: Optional[Workspace] = None,
                  grad: Optional[torch.Tensor] = None, loss_out: Optional[torch.Tensor] = None,
-                 surface: Optional[torch.Tensor] = None, want_loss: bool = True, stream=None):
+                 surface: Optional[torch.Tensor] = None, want_loss: bool = True, stream=None,
+                 periodic: bool = False):
     """graf_af_loss_grad -> (loss[B] float64, grad[B,N] complex64 = dL/ds*, surface or None)."""
     s = _check_s(s)
-    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard)
+    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic)
     ld = loss.desc()
     B, N = s.shape
     if grad is None:
@@ -155,13 +160,14 @@ def af_loss_grad(s: torch.Tensor, M: int, loss: LossSpec, *, global_partials: Op
 
 
 def af_backward(s: torch.Tensor, M: int, dA: torch.Tensor, *, k_begin=None, k_end=None,
-                layout: str = "centered", ws: Optional[Workspace] = None, stream=None) -> torch.Tensor:
+                layout: str = "centered", ws: Optional[Workspace] = None, stream=None,
+                periodic: bool = False) -> torch.Tensor:
     """graf_af_backward: dL/ds* from dA = dL/dA* over rows [k_begin, k_end)."""
     s = _check_s(s)
     if dA.dtype != torch.complex64 or not dA.is_cuda:
         raise TypeError("graf: dA must be a complex64 CUDA tensor")
     dA = dA.contiguous()
-    d = _desc(s, M, None, layout, k_begin, k_end)
+    d = _desc(s, M, None, layout, k_begin, k_end, periodic=periodic)
     B, N = s.shape
     if dA.shape != (B, d.k_end - d.k_begin, M):
         raise ValueError(f"dA shape {tuple(dA.shape)} != {(B, d.k_end - d.k_begin, M)}")
@@ -197,28 +203,30 @@ class AF(torch.autograd.Function):
     """Differentiable complex surface A (rows [k_begin,k_end), layout)."""
 
     @staticmethod
-    def forward(ctx, s, M, layout="centered", k_begin=None, k_end=None):
-        surf, _ = af_forward(s.detach(), M, out="c64", layout=layout, k_begin=k_begin, k_end=k_end)
+    def forward(ctx, s, M, layout="centered", k_begin=None, k_end=None, periodic=False):
+        surf, _ = af_forward(s.detach(), M, out="c64", layout=layout, k_begin=k_begin, k_end=k_end,
+                             periodic=periodic)
         ctx.save_for_backward(s)
-        ctx.cfg = (M, layout, k_begin, k_end, s.dim())
+        ctx.cfg = (M, layout, k_begin, k_end, s.dim(), periodic)
         return surf if s.dim() == 2 else surf[0]
 
     @staticmethod
     def backward(ctx, grad_out):
         (s,) = ctx.saved_tensors
-        M, layout, kb, ke, dim = ctx.cfg
+        M, layout, kb, ke, dim, periodic = ctx.cfg
         g = grad_out if dim == 2 else grad_out[None]
         # torch hands 2*dL/dA*; the adjoint is linear, so the result is torch's 2*dL/ds*.
-        gs = af_backward(s.detach(), M, g.to(torch.complex64), k_begin=kb, k_end=ke, layout=layout)
-        return (gs if dim == 2 else gs[0]), None, None, None, None
+        gs = af_backward(s.detach(), M, g.to(torch.complex64), k_begin=kb, k_end=ke, layout=layout,
+                         periodic=periodic)
+        return (gs if dim == 2 else gs[0]), None, None, None, None, None
 
 
 class AFLoss(torch.autograd.Function):
     """Per-waveform loss L_b (float64 [B]) with the fused kernels' gradient."""
 
     @staticmethod
-    def forward(ctx, s, M, spec):
-        lo, g, _ = af_loss_grad(s.detach(), M, spec)
+    def forward(ctx, s, M, spec, periodic=False):
+        lo, g, _ = af_loss_grad(s.detach(), M, spec, periodic=periodic)
         ctx.save_for_backward(g)
         ctx.dim = s.dim()
         return lo if s.dim() == 2 else lo[0]
@@ -228,12 +236,12 @@ class AFLoss(torch.autograd.Function):
         (g,) = ctx.saved_tensors
         go = grad_out if ctx.dim == 2 else grad_out[None]
         gs = 2.0 * go.to(torch.float32)[:, None] * g          # torch .grad = 2 dL/ds*
-        return (gs if ctx.dim == 2 else gs[0]), None, None
+        return (gs if ctx.dim == 2 else gs[0]), None, None, None
 
 
-def af(s, M, layout="centered", k_begin=None, k_end=None):
-    return AF.apply(s, M, layout, k_begin, k_end)
+def af(s, M, layout="centered", k_begin=None, k_end=None, periodic=False):
+    return AF.apply(s, M, layout, k_begin, k_end, periodic)
 
 
-def af_loss(s, M, spec: LossSpec):
-    return AFLoss.apply(s, M, spec)
+def af_loss(s, M, spec: LossSpec, periodic=False):
+    return AFLoss.apply(s, M, spec, periodic)

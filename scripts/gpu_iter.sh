@@ -10,3 +10,5 @@ fi
 bash scripts/bench_all.sh $TAG $CFGS
 timeout 600 python bench.py --config 3 --mode forward --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c3fwd.json 2> gpurun_out/bench_${TAG}_c3fwd.err
 python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c3fwd.json')); r=d['roofline']; print('c3fwd', d['ms_per_step'], r['bound'], r['frac'])"
+timeout 600 python bench.py --config 2 --periodic --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c2per.json 2> gpurun_out/bench_${TAG}_c2per.err
+python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c2per.json')); r=d['roofline']; print('c2per', d['ms_per_step'], r['bound'], r['frac'])"
