@@ -52,7 +52,8 @@ __all__ = [
     "LossSpec", "energy", "delay_rows", "centred_bins", "dft_matrix",
     "lag_products", "ambiguity", "region", "loss_terms", "loss",
     "loss_and_grad", "adjoint", "correlate", "surface", "loss_and_grad_chunked",
-    "periodic_ambiguity",
+    "periodic_ambiguity", "hard_psl_and_grad", "spectral_variance_and_grad", "phase_grad",
+    "adam_step", "lpi_loss_and_grad",
 ]
 
 
@@ -359,3 +360,83 @@ def periodic_ambiguity(s: np.ndarray) -> np.ndarray:
     n = s.shape[0]
     R = np.stack([s * np.conj(np.roll(s, k)) for k in range(n)])
     return R @ dft_matrix(n, n, np.arange(n), sign=+1)
+
+
+# ---------------------------------------------------------------------------
+# The paper's §7 workload: hard PSL with its argmax
+# subgradient (Eq. 19), spectral variance, the Eq. 26
+# loss L = PSL + lambda*alpha*SV on phase-coded waveforms
+# s = exp(j*theta), and the Adam update.
+# ---------------------------------------------------------------------------
+def hard_psl_and_grad(s: np.ndarray, M: int, spec: LossSpec, periodic: bool = False):
+    """PSL = max_{Omega_s} x (x = chi/E^2 normalized | chi raw) and its subgradient
+    dPSL/ds* at the argmax cell (Eq. 19; ties -> lowest row-major index over
+    (delay k ascending, raw Doppler bin m ascending), reading R23).  Returns
+    (psl, g, (k, m))."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    rows, bins, mask, _ = region(n, M, spec, periodic)
+    E = energy(s)
+    A = ambiguity(s, M, rows, bins, periodic)
+    chi = A.real ** 2 + A.imag ** 2
+    x = chi / E ** 2 if spec.normalize else chi
+    # row-major order over (k ascending, m ascending): sort the bins
+    order = np.argsort(bins, kind="stable")
+    xs = np.where(mask, x, -np.inf)[:, order]
+    flat = int(np.argmax(xs))                     # first occurrence = lowest index
+    i, jj = divmod(flat, len(bins))
+    j = int(order[jj])
+    psl = float(x[i, j])
+    G = np.zeros_like(A)
+    G[i, j] = A[i, j] / E ** 2 if spec.normalize else A[i, j]   # d x/d A* at the cell
+    g = adjoint(s, M, G, rows, bins, periodic)
+    if spec.normalize:
+        g = g - (2.0 / E ** 3) * chi[i, j] * s
+    return psl, g, (int(rows[i]), int(bins[j]))
+
+
+def spectral_variance_and_grad(s: np.ndarray):
+    """SV = var{|F s|^2 / sum |F s|^2} over the N DFT bins (the paper's
+    PyTorch var: unbiased, N - 1 in the denominator, reading R22), F = length-N DFT
+    written as its matrix; and dSV/ds* (chain rule through p_j = |S_j|^2 / P)."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    F = dft_matrix(n, n, np.arange(n)).T          # S_j = sum_n s_n exp(-2 pi i j n / N)
+    S = F @ s
+    pw = S.real ** 2 + S.imag ** 2
+    P = float(np.sum(pw))
+    p = pw / P
+    mean = float(np.mean(p))
+    sv = float(np.sum((p - mean) ** 2) / (n - 1))
+    c = 2.0 * (p - mean) / (n - 1)                # dSV/dp_j
+    dS = (c - float(np.sum(c * p))) * S / P       # dSV/dS_j*
+    g = np.conj(F).T @ dS                         # adjoint of S = F s
+    return sv, g
+
+
+def phase_grad(s: np.ndarray, g: np.ndarray) -> np.ndarray:
+    """dL/dtheta for s = exp(j*theta) and g = dL/ds*: 2 Re(conj(g) * j s) = -2 Im(s conj(g))."""
+    return -2.0 * np.imag(np.asarray(s) * np.conj(np.asarray(g)))
+
+
+def adam_step(theta, m, v, grad, t: int, lr: float = 0.01, beta1: float = 0.9,
+              beta2: float = 0.999, eps: float = 1e-8):
+    """One Adam update (Kingma & Ba, Alg. 1; P:L425 'Adam optimizer with learning
+    rate 0.01'), step t >= 1.  Returns (theta, m, v)."""
+    m = beta1 * m + (1.0 - beta1) * grad
+    v = beta2 * v + (1.0 - beta2) * grad * grad
+    mh = m / (1.0 - beta1 ** t)
+    vh = v / (1.0 - beta2 ** t)
+    return theta - lr * mh / (np.sqrt(vh) + eps), m, v
+
+
+def lpi_loss_and_grad(theta: np.ndarray, spec: LossSpec, lam: float, alpha: float = 2000.0,
+                      periodic: bool = True):
+    """Eq. 26: L = PSL + lam*alpha*SV on s = exp(j*theta) (M = N), and dL/dtheta."""
+    theta = np.asarray(theta, dtype=np.float64)
+    s = np.exp(1j * theta)
+    n = s.shape[0]
+    psl, gp, _ = hard_psl_and_grad(s, n, spec, periodic)
+    sv, gs = spectral_variance_and_grad(s)
+    L = psl + lam * alpha * sv
+    return L, phase_grad(s, gp + lam * alpha * gs), dict(psl=psl, sv=sv)

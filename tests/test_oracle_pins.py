@@ -430,3 +430,87 @@ def test_periodic_adjoint_inner_product_identity():
     lhs = np.vdot(G, lin).real
     rhs = np.vdot(O.adjoint(s, n, G, rows, periodic=True), dlt).real
     assert abs(lhs - rhs) < 1e-11 * max(1, abs(lhs))
+
+
+# ---------------------------------------------------------------- the paper's §7 workload (NEXT-2)
+def _fd(fun, x, eps=1e-6, complex_input=True):
+    g = np.zeros(len(x), complex if complex_input else float)
+    for p in range(len(x)):
+        units = (1.0, 1j) if complex_input else (1.0,)
+        for u in units:
+            xp = x.copy(); xp[p] += eps * u
+            xm = x.copy(); xm[p] -= eps * u
+            g[p] += (fun(xp) - fun(xm)) / (2 * eps) * (1.0 if u == 1.0 else 1j)
+    return g
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("normalize", [1, 0])
+def test_hard_psl_value_and_subgradient(periodic, normalize):
+    n = 8
+    s = rs(n, 90 + normalize)
+    spec = O.LossSpec(k_max=3, d_max=3, ml_k=0, ml_d=0, normalize=normalize)
+    psl, g, (k, m) = O.hard_psl_and_grad(s, n, spec, periodic)
+    t = O.loss_terms(s, n, spec, periodic)
+    assert psl == t["x"][t["mask"]].max()                      # Eq. 19: the max over Omega_s
+    # away from ties the max is differentiable: central differences of PSL
+    fd = _fd(lambda z: O.hard_psl_and_grad(z, n, spec, periodic)[0], s)
+    np.testing.assert_allclose(2 * g, fd, atol=1e-6 * max(1.0, np.abs(fd).max()))
+
+
+def test_hard_psl_mirrored_tie_and_barker():
+    # |A[-k,-m]| = |A[k,m]|: the max is attained twice; the subgradient of either cell is the same
+    s = rs(10, 95)
+    spec = O.LossSpec(k_max=9, d_max=8, normalize=1)
+    psl, g, (k, m) = O.hard_psl_and_grad(s, 16, spec)
+    assert k <= 0                                              # row-major first of the mirrored pair
+    # Barker-13 zero-Doppler: max aperiodic sidelobe 1 -> PSL = 1/169 on the delay axis (golden)
+    b = barker13().astype(complex)
+    psl, _, (k, m) = O.hard_psl_and_grad(b, 16, O.LossSpec(k_max=12, d_max=0, normalize=1))
+    assert abs(psl - 1 / 169) < 1e-15 and m == 0
+
+
+def test_spectral_variance_closed_forms_and_gradient():
+    n = 16
+    # impulse: flat spectrum -> SV = 0 with zero gradient at the minimum
+    d = np.zeros(n, complex); d[3] = 1.0
+    sv, g = O.spectral_variance_and_grad(d)
+    assert abs(sv) < 1e-30 and np.abs(g).max() < 1e-15
+    # single tone: all power in one bin -> p = e_j, var = ((1 - 1/N)^2 + (N-1)/N^2)/(N-1) = 1/N
+    tone = np.exp(2j * np.pi * 5 * np.arange(n) / n)
+    sv, _ = O.spectral_variance_and_grad(tone)
+    assert abs(sv - 1.0 / n) < 1e-14
+    # matches numpy.fft + an unbiased variance on random input; central differences
+    s = rs(n, 96)
+    S = np.fft.fft(s)
+    p = np.abs(S) ** 2 / np.sum(np.abs(S) ** 2)
+    sv, g = O.spectral_variance_and_grad(s)
+    assert abs(sv - np.var(p, ddof=1)) < 1e-15
+    fd = _fd(lambda z: O.spectral_variance_and_grad(z)[0], s)
+    np.testing.assert_allclose(2 * g, fd, atol=1e-7 * np.abs(fd).max())
+    assert abs(np.vdot(g, s)) < 1e-12                           # scale- and phase-invariant
+
+
+def test_adam_matches_torch_and_first_step():
+    r = SplitMix64(97)
+    th = r.uniform(12) * 6.0
+    grads = [r.uniform(12) - 0.5 for _ in range(5)]
+    p = torch.tensor(th, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.Adam([p], lr=0.01)
+    m = np.zeros(12); v = np.zeros(12); x = th.copy()
+    for t, gr in enumerate(grads, start=1):
+        opt.zero_grad(); p.grad = torch.tensor(gr); opt.step()
+        x, m, v = O.adam_step(x, m, v, gr, t)
+        np.testing.assert_allclose(x, p.detach().numpy(), rtol=0, atol=1e-14)
+    x1, _, _ = O.adam_step(th, np.zeros(12), np.zeros(12), grads[0], 1)
+    np.testing.assert_allclose(x1, th - 0.01 * np.sign(grads[0]), atol=1e-9)   # |step| = lr at t = 1
+
+
+def test_lpi_phase_gradient_central_differences():
+    n = 8
+    th = SplitMix64(98).uniform(n) * 2 * np.pi
+    spec = O.LossSpec(k_max=n, d_max=n, normalize=1)
+    L, gth, parts = O.lpi_loss_and_grad(th, spec, lam=0.5)
+    fd = _fd(lambda z: O.lpi_loss_and_grad(z, spec, lam=0.5)[0], th, complex_input=False)
+    np.testing.assert_allclose(gth, fd.real, atol=1e-6 * max(1.0, np.abs(fd).max()))
+    assert abs(L - (parts["psl"] + 0.5 * 2000.0 * parts["sv"])) < 1e-15 * max(1, L)
