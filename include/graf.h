@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GRAF_ABI_VERSION 2
+#define GRAF_ABI_VERSION 3
 #define GRAF_MAX_M 16384
 
 typedef enum {
@@ -107,14 +107,20 @@ typedef struct {
   float lambda_isl, lambda_psl;
   float temperature;        /* T > 0 (read iff lambda_psl != 0) */
   int32_t normalize;        /* 1 (default reading R6) or 0 (raw chi) */
+  float lambda_hpsl;        /* weight of the HARD PSL = max_{Omega} x (Eq. 19) with its
+                               argmax subgradient (the paper's section-7 loss, L416); ties go to
+                               the lowest row-major (delay, raw Doppler bin) cell (reading R23).
+                               Needs the global max, so it runs pass 1 like soft-PSL.  (ABI v3) */
 } graf_loss_desc;
 
 /* Per-waveform partial sums over the rows a call covered (exactly combinable
  * across delay shards with graf_combine_partials):
- *   isl_sum = sum w*chi (raw numerator);  lse_max = max x;
+ *   isl_sum = sum w*chi (raw numerator);  lse_max = max x (= the hard PSL);
  *   lse_sum = sum exp((x - lse_max)/T);   cen_sum = sum expm1((x - xbar)/T) with
- *   xbar = (M-1)/|Omega| when Omega is constant-sum (reading R13), else 0. */
-typedef struct { double isl_sum, lse_max, lse_sum, cen_sum; } graf_partials;
+ *   xbar = (M-1)/|Omega| when Omega is constant-sum (reading R13), else 0;
+ *   psl_key = row-major key (delay index * M + raw Doppler bin, delays ascending from
+ *   the smallest delay of the region) of the argmax cell (lambda_hpsl != 0 only). */
+typedef struct { double isl_sum, lse_max, lse_sum, cen_sum, psl_key, reserved; } graf_partials;
 
 int32_t graf_abi_version(void);
 const char* graf_status_string(graf_status status);
@@ -150,6 +156,31 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
  * ("IFFT operation (linear)", Eq. 15).  Linear in dA. */
 graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA,
                              void* grad, void* ws, size_t ws_bytes, void* stream);
+
+/* Spectral variance of each waveform (the paper's section-7 LPI term, L417):
+ *   SV_b = var{ |F s_b|^2 / sum |F s_b|^2 } over the N DFT bins, unbiased (N - 1;
+ *   the paper's PyTorch var, reading R22), F the length-N DFT,
+ * and its Wirtinger gradient dSV/ds*.  Writes weight*SV_b into loss[b] and
+ * weight*dSV/ds* into grad[b][:], or ADDS them when accumulate = 1 (to combine
+ * with a graf_af_loss_grad result: the Eq. 26 loss PSL + lambda*alpha*SV).
+ * weights: device float [B] per-waveform weights (e.g. lambda_b * alpha for a
+ * batched lambda sweep), or NULL to use `weight` for every waveform.
+ * s, grad: complex64 [B][N]; loss: double [B] (nullable).  N a power of two,
+ * 2 <= N <= 16384.  No workspace. */
+graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, float weight,
+                                   const float* weights, double* loss, void* grad, int32_t accumulate,
+                                   void* stream);
+
+/* One Adam step (L425: Adam, learning rate 0.01) on the phases of phase-coded
+ * waveforms s = exp(j*theta):  dL/dtheta = -2 Im(s conj(g)) from g = dL/ds*
+ * (complex64 [B][N]); m, v: float [B][N] moments; step: int32 [B] completed steps
+ * per waveform (incremented here, so a captured CUDA graph can replay the step);
+ * theta updated in place; s_out (complex64 [B][N], may alias nothing else) gets
+ * exp(j*theta_new).  Torch's Adam: m = b1 m + (1-b1) d, v = b2 v + (1-b2) d^2,
+ * theta -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps). */
+graf_status graf_phase_adam_step(int64_t batch, int32_t n, float* theta, float* m, float* v,
+                                 int32_t* step, const void* grad, void* s_out, float lr, float beta1,
+                                 float beta2, float eps, void* stream);
 
 /* Combine per-shard partials shards[G][B] into out[B] in shard order
  * (deterministic).  on_device = 1: both arrays are device pointers and the work

@@ -2,11 +2,13 @@
 
 Public API (thin binding of include/graf.h; all compute in libgraf.so):
     af_forward, af_loss_grad, af_backward, combine_partials, LossSpec,
-    af / af_loss (torch autograd), sharding.* (torch.distributed layers).
+    af / af_loss (torch autograd), sharding.* (torch.distributed layers),
+    spectral_variance, phase_adam_step, LpiOptimizer (the paper's section-7 workload).
 """
 from ._lib import GrafError, lib  # noqa: F401
-from .graf import (AF, AFLoss, LossSpec, af, af_backward, af_forward, af_loss,  # noqa: F401
-                   af_loss_grad, combine_partials, workspace_bytes)
+from .graf import (AF, AFLoss, LossSpec, LpiOptimizer, af, af_backward, af_forward, af_loss,  # noqa: F401
+                   af_loss_grad, combine_partials, phase_adam_step, spectral_variance, workspace_bytes)
 
 __all__ = ["AF", "AFLoss", "LossSpec", "af", "af_backward", "af_forward", "af_loss", "af_loss_grad",
-           "combine_partials", "workspace_bytes", "GrafError", "lib"]
+           "combine_partials", "workspace_bytes", "GrafError", "lib", "spectral_variance", "phase_adam_step",
+           "LpiOptimizer"]

@@ -10,14 +10,15 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # GRAF_LIB_PATH: tuning builds only (scripts/tune.py); the default is the in-tree library.
 LIB_PATH = os.environ.get("GRAF_LIB_PATH") or os.path.join(PKG, "libgraf.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_ENONFINITE, GRAF_EWORKSPACE = range(6)
 OUT_NONE, OUT_C64, OUT_ABS_F32, OUT_POW_F32 = range(4)
 DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
 
 EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_workspace_bytes",
            "graf_af_forward", "graf_af_loss_grad", "graf_af_backward", "graf_combine_partials",
-           "graf_set_profile_events", "graf_last_launch_count")
+           "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
+           "graf_phase_adam_step")
 
 
 class AfDesc(ctypes.Structure):
@@ -31,11 +32,12 @@ class LossDesc(ctypes.Structure):
     _fields_ = [("k_max", c_int32), ("d_max", c_int32), ("ml_k", c_int32), ("ml_d", c_int32),
                 ("w_k", c_void_p), ("w_d", c_void_p),
                 ("lambda_isl", c_float), ("lambda_psl", c_float), ("temperature", c_float),
-                ("normalize", c_int32)]
+                ("normalize", c_int32), ("lambda_hpsl", c_float)]
 
 
 class Partials(ctypes.Structure):
-    _fields_ = [("isl_sum", c_double), ("lse_max", c_double), ("lse_sum", c_double), ("cen_sum", c_double)]
+    _fields_ = [("isl_sum", c_double), ("lse_max", c_double), ("lse_sum", c_double), ("cen_sum", c_double),
+                ("psl_key", c_double), ("reserved", c_double)]
 
 
 class GrafError(RuntimeError):
@@ -73,6 +75,12 @@ def lib() -> ctypes.CDLL:
         L.graf_combine_partials.restype = c_int32
         L.graf_combine_partials.argtypes = [POINTER(LossDesc), c_void_p, c_int32, c_int64, c_void_p, c_int32,
                                             c_void_p]
+        L.graf_spectral_variance.restype = c_int32
+        L.graf_spectral_variance.argtypes = [c_int64, c_int32, c_void_p, c_float, c_void_p, c_void_p, c_void_p,
+                                             c_int32, c_void_p]
+        L.graf_phase_adam_step.restype = c_int32
+        L.graf_phase_adam_step.argtypes = [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                           c_void_p, c_float, c_float, c_float, c_float, c_void_p]
         L.graf_last_launch_count.restype = c_int32
         L.graf_last_launch_count.argtypes = []
         L.graf_set_profile_events.restype = c_int32

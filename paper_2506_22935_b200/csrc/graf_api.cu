@@ -167,7 +167,7 @@ graf_status check_loss(const graf_af_desc* af, const graf_loss_desc* L) {
     return fail(GRAF_EINVAL, "negative region bound");
   if (L->normalize != 0 && L->normalize != 1) return fail(GRAF_EINVAL, "normalize must be 0 or 1");
   if (L->lambda_psl != 0.f && !(L->temperature > 0.f)) return fail(GRAF_EINVAL, "temperature must be > 0");
-  if (!std::isfinite(L->lambda_isl) || !std::isfinite(L->lambda_psl))
+  if (!std::isfinite(L->lambda_isl) || !std::isfinite(L->lambda_psl) || !std::isfinite(L->lambda_hpsl))
     return fail(GRAF_EINVAL, "non-finite lambda");
   const int kl = std::min(L->k_max, af->periodic ? af->n / 2 : af->n - 1);
   const int dl = std::min(L->d_max, af->m / 2);
@@ -456,6 +456,8 @@ void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
   const bool full = rp.kloss == (af->periodic ? N / 2 : N - 1) && L->d_max >= M / 2 && L->ml_k == 0 && L->ml_d == 0;
   rp.centred = (L->normalize && !L->w_k && !L->w_d && full && L->lambda_psl != 0.f) ? 1 : 0;
   rp.omega = (double)(af->periodic ? N : 2 * N - 1) * M - 1.0;   // |Omega| of the full plane
+  rp.want_argmax = L->lambda_hpsl != 0.f ? 1 : 0;
+  rp.key_lo = (af->periodic && 2 * rp.kloss == N) ? -rp.kloss + 1 : -rp.kloss;
   rp.xbar = (float)((M - 1) / rp.omega);
 }
 
@@ -581,6 +583,33 @@ graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L,
   return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "partials_reduce_kernel launch");
 }
 
+// hard PSL term (loss and argmax subgradient) from the combined partials
+graf_status run_psl(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, const void* s,
+                    const graf_partials* stats, double* loss_out, void* grad, int accumulate, cudaStream_t st) {
+  (void)pl;
+  PslParams q;
+  std::memset(&q, 0, sizeof(q));
+  const int N = af->n;
+  const int kl = std::min(L->k_max, af->periodic ? N / 2 : N - 1);
+  q.s = static_cast<const float2*>(s);
+  q.stats = stats;
+  q.N = N;
+  q.M = af->m;
+  q.key_lo = (af->periodic && 2 * kl == N) ? -kl + 1 : -kl;
+  q.periodic = af->periodic;
+  q.normalize = L->normalize;
+  q.lam = L->lambda_hpsl;
+  q.add_grad = (af->shard_index == 0) ? 1 : 0;
+  q.accumulate = accumulate;
+  q.loss = loss_out;
+  q.grad = static_cast<float2*>(grad);
+  psl_grad_kernel<<<(unsigned)af->batch, 256, 0, st>>>(q);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "psl_grad_kernel launch");
+  ++t_launches;
+  return GRAF_OK;
+}
+
 }  // namespace
 }  // namespace graf
 
@@ -676,7 +705,10 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
   graf_partials* comb = reinterpret_cast<graf_partials*>(static_cast<char*>(ws) + pl.off_comb);
   const graf_partials* stats = global;
-  if (loss->lambda_psl == 0.f) {
+  const bool hpsl = loss->lambda_hpsl != 0.f;       // hard PSL (section-7 loss), reading R23
+  const bool soft = loss->lambda_psl != 0.f;
+  const bool dense = loss->lambda_isl != 0.f || soft;   // terms with a per-cell f'
+  if (!soft && !hpsl) {
     // single fused pass (f' = lambda_isl * w known up front); unsharded calls also
     // fuse the finalize into the row kernel when a waveform's CTAs fit one cluster
     pl.fuse_req = (global == nullptr);
@@ -699,23 +731,27 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
       stats = comb;
     }
     rp.stats = stats;
-    if (pl.U > 0) {
+    if (pl.U > 0 && dense) {
       e = launch_rows(pl, rp, (int)af->batch, cs, K_PASS2);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 2) launch");
-      prof_mark(false, cs);
     }
+    if (pl.U > 0) prof_mark(false, cs);
   }
   if (pl.U == 0) {
-    if (loss_out) {
+    if (loss_out && dense) {
       // no rows here: loss purely from the global partials
       Plan p0 = pl;
       p0.P = 0;
-      return run_finalize(af, loss, p0, s, ws, global, loss_out, nullptr, false, cs);
+      if ((st = run_finalize(af, loss, p0, s, ws, global, loss_out, nullptr, false, cs))) return st;
     }
+    if (hpsl) return run_psl(af, loss, pl, s, stats, loss_out, grad, dense ? 1 : 0, cs);
     return GRAF_OK;
   }
-  if (pl.fused) return GRAF_OK;
-  return run_finalize(af, loss, pl, s, ws, stats, loss_out, grad, true, cs);
+  if (!pl.fused && dense) {
+    if ((st = run_finalize(af, loss, pl, s, ws, stats, loss_out, grad, true, cs))) return st;
+  }
+  if (hpsl) return run_psl(af, loss, pl, s, stats, loss_out, grad, dense ? 1 : 0, cs);
+  return GRAF_OK;
 }
 
 graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
@@ -762,7 +798,7 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
     return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "combine_partials_kernel launch");
   }
   for (int64_t b = 0; b < B; ++b) {
-    double S = 0, Z = 0, Cs = 0;
+    double S = 0, Z = 0, Cs = 0, key = (double)0x7fffffff;
     double m = -INFINITY;
     for (int q = 0; q < G; ++q) {
       const graf_partials& g = shards[(size_t)q * B + b];
@@ -770,6 +806,7 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
       Cs += g.cen_sum;
       const double m2 = g.lse_max;
       const double Z2 = g.lse_sum;
+      if (m2 > m || (m2 == m && g.psl_key < key)) key = g.psl_key;
       if (m2 == -INFINITY) continue;
       if (m == -INFINITY) {
         m = m2;
@@ -781,8 +818,65 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
         Z = Z + Z2 * std::exp((m2 - m) / (double)T);
       }
     }
-    out[b] = graf_partials{S, m, Z, Cs};
+    out[b] = graf_partials{S, m, Z, Cs, key, 0.0};
   }
+  return GRAF_OK;
+}
+
+graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, float weight,
+                                   const float* weights, double* loss, void* grad, int32_t accumulate,
+                                   void* stream) {
+  t_launches = 0;
+  if (batch < 1 || batch > (1LL << 31) - 1) return fail(GRAF_EINVAL, "batch = %lld", (long long)batch);
+  if (!is_pow2(n) || n < 2) return fail(GRAF_EINVAL, "N = %d is not a power of two >= 2", n);
+  if (n > GRAF_MAX_M) return fail(GRAF_EUNSUPPORTED, "N = %d > %d", n, GRAF_MAX_M);
+  if (!s || !grad || !aligned8(s) || !aligned8(grad)) return fail(GRAF_EINVAL, "s / grad NULL or misaligned");
+  if (!std::isfinite(weight)) return fail(GRAF_EINVAL, "non-finite weight");
+  cudaError_t e = ensure_twiddles();
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  SvParams q{static_cast<const float2*>(s), n, weight, weights, accumulate ? 1 : 0, loss,
+             static_cast<float2*>(grad)};
+  if (n <= 1024) {
+    const int threads = std::max(32, n);
+    const size_t smem = sizeof(float2) * 2 * (size_t)n + sizeof(double) * threads;
+    sv_direct_kernel<<<(unsigned)batch, threads, smem, cs>>>(q);
+  } else {
+    auto go = [&](auto kern, int T, int XS) -> cudaError_t {
+      const size_t smem = sizeof(float2) * (size_t)((XS + 1) & ~1) + sizeof(double) * T;
+      cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (ea != cudaSuccess) return ea;
+      kern<<<(unsigned)batch, T, smem, cs>>>(q);
+      return cudaSuccess;
+    };
+    switch (n) {
+      case 2048: e = go(sv_fft_kernel<2048>, Cfg<2048>::T, Cfg<2048>::XS); break;
+      case 4096: e = go(sv_fft_kernel<4096>, Cfg<4096>::T, Cfg<4096>::XS); break;
+      case 8192: e = go(sv_fft_kernel<8192>, Cfg<8192>::T, Cfg<8192>::XS); break;
+      default: e = go(sv_fft_kernel<16384>, Cfg<16384>::T, Cfg<16384>::XS); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "sv_fft_kernel attribute");
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "spectral variance kernel launch");
+  ++t_launches;
+  return GRAF_OK;
+}
+
+graf_status graf_phase_adam_step(int64_t batch, int32_t n, float* theta, float* m, float* v, int32_t* step,
+                                 const void* grad, void* s_out, float lr, float beta1, float beta2, float eps,
+                                 void* stream) {
+  t_launches = 0;
+  if (batch < 1 || batch > (1LL << 31) - 1 || n < 1) return fail(GRAF_EINVAL, "batch / N out of range");
+  if (!theta || !m || !v || !step || !grad || !s_out) return fail(GRAF_EINVAL, "NULL argument");
+  if (!(lr > 0.f) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f))
+    return fail(GRAF_EINVAL, "Adam hyper-parameters out of range");
+  AdamParams a{theta, m, v, step, static_cast<const float2*>(grad), static_cast<float2*>(s_out), n,
+               lr, beta1, beta2, eps};
+  phase_adam_kernel<<<(unsigned)batch, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "phase_adam_kernel launch");
+  ++t_launches;
   return GRAF_OK;
 }
 

@@ -217,7 +217,11 @@ struct Twiddles {
   static constexpr int NP = num_passes(M, E);
   static constexpr int NB = tw_offset(M, E, NP);          // base twiddles per thread
   static constexpr int NTW = tw_count(M, E);              // all twiddles per thread
+#ifdef GRAF_NO_TWCACHE
+  static constexpr bool CACHE = false;
+#else
   static constexpr bool CACHE = (NTW > 0 && NTW <= 16);   // keep every power in registers
+#endif
   // pass-1 powers from a shared-memory table tw1[(r - 1) * NS1 + jm] (NS1 = first radix;
   // every thread of a slot shares the NS1 rows, so reads are broadcast / conflict-free)
   static constexpr bool SMEM1 = !CACHE && NP >= 2;

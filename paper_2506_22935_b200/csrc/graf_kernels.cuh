@@ -61,6 +61,10 @@ struct RowParams {
   int stg_floats;      // staging floats per row slot (2*M*{1,2}: rows +k and -k)
   int gpad;            // 1: left-padded gradient accumulators (M == N, folded rows)
   int periodic;        // 1: circular lag products (the paper's Eq. 2 / Alg. 1), M == N
+  // hard PSL (K_FWD): track the argmax cell of x over the region as a row-major key
+  // (delay index from key_lo) * M + raw Doppler bin, ties -> lowest key (reading R23)
+  int want_argmax;
+  int key_lo;
   // fused finalize (K_ISL, P <= 8 CTAs per waveform launched as one thread-block
   // cluster): cluster rank 0 combines the CTAs' partials over distributed shared
   // memory and writes loss and grad directly (no partial records, no finalize kernel)
@@ -217,6 +221,47 @@ __device__ __forceinline__ float block_max_all(float v, double* scratch) {
     __syncthreads();
     return r;  // in every thread
   }
+}
+
+// CTA argmax of (value, key) pairs: largest value, ties -> smallest key; the key of
+// the winner in thread 0 (fixed shuffle tree and warp order: deterministic)
+template <int THREADS>
+__device__ __forceinline__ int block_argmax_key(float x, int key, double* scratch) {
+  constexpr int NW = (THREADS + 31) / 32;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ox = __shfl_xor_sync(0xffffffffu, x, off);
+    const int ok = __shfl_xor_sync(0xffffffffu, key, off);
+    if (ox > x || (ox == x && ok < key)) {
+      x = ox;
+      key = ok;
+    }
+  }
+  if constexpr (NW == 1) {
+    return key;
+  } else {
+    float* sx = reinterpret_cast<float*>(scratch);
+    int* sk = reinterpret_cast<int*>(scratch) + 32;
+    if ((threadIdx.x & 31) == 0) {
+      sx[threadIdx.x >> 5] = x;
+      sk[threadIdx.x >> 5] = key;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < NW; ++w)
+        if (sx[w] > x || (sx[w] == x && sk[w] < key)) {
+          x = sx[w];
+          key = sk[w];
+        }
+    }
+    __syncthreads();
+    return key;
+  }
+}
+
+// argmax-key merge that goes with lse_merge: called BEFORE lse_merge updates m
+__device__ __forceinline__ void key_merge(double m, double& key, double m2, double key2) {
+  if (m2 > m || (m2 == m && key2 < key)) key = key2;
 }
 
 // exact merge of (max, sum exp((x - max)/T)) pairs, in double (maxima are exact floats)
@@ -496,6 +541,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // per-thread accumulators (double across rows, float within a row)
   double accS = 0.0, accZ = 0.0, accC = 0.0, accF = 0.0;
   float accM = -INFINITY;
+  float argX = -INFINITY;   // hard-PSL argmax (value, key) of this thread
+  int argK = 0x7fffffff;
 
   const int rows_per_iter = P * S;
   const int iters = (p.U + rows_per_iter - 1) / rows_per_iter;
@@ -674,7 +721,18 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
           rowS = fmaf(in ? w : 0.f, chi, rowS);
           if constexpr (KIND == K_FWD) {
-            rowM = fmaxf(rowM, in ? (p.normalize ? chi * invE2 : chi) : -INFINITY);
+            const float x = p.normalize ? chi * invE2 : chi;
+            rowM = fmaxf(rowM, in ? x : -INFINITY);
+            if (p.want_argmax) {
+              // canonical (row-major first) cell of the mirrored pair holding this value
+              const int m = t + e * T;
+              const int mm = (M - m) & (M - 1);
+              const bool self = (k == 0) || (p.periodic && 2 * k == N);
+              const int key = self ? (k - p.key_lo) * M + min(m, mm) : (-k - p.key_lo) * M + mm;
+              const bool better = in && (x > argX || (x == argX && key < argK));
+              argX = better ? x : argX;
+              argK = better ? key : argK;
+            }
           } else if constexpr (KIND == K_ISL) {
             v[e] = cscale(v[e], in ? p.lam_isl * w * gsc : 0.f);   // G (x2 for a folded row pair)
           } else {
@@ -683,7 +741,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             if (use_centred) {
               fp = p.lam_psl * (expm1_fast((x - p.xbar) * p.invT) - ebar) * invZc;
             } else {
-              fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);
+              fp = p.lam_isl * w;
+              if (p.lam_psl != 0.f) fp += p.lam_psl * exp_fast((x - lse) * p.invT);
             }
             fp = in ? fp : 0.f;
             rowF = fmaf(fp, chi, rowF);
@@ -843,12 +902,17 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         C0 = block_sum<THREADS>(accC, scratch);
       }
     }
+    int K0 = 0x7fffffff;
+    if constexpr (KIND == K_FWD) {
+      if (p.want_argmax) K0 = block_argmax_key<THREADS>(argX, argK, scratch);
+    }
     if (threadIdx.x == 0) {
       rec[0] = S0;
       rec[1] = (double)M0;
       rec[2] = Z0;
       rec[3] = C0;
       rec[4] = F0;
+      rec[5] = (double)K0;
     }
   } else {
     if (threadIdx.x == 0) {
@@ -857,6 +921,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       rec[2] = 0.0;
       rec[3] = 0.0;
       rec[4] = 0.0;
+      rec[5] = (double)0x7fffffff;
     }
   }
 
@@ -937,12 +1002,13 @@ struct ReduceParams {
 __global__ void partials_reduce_kernel(ReduceParams r) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= r.B) return;
-  double S = 0, Z = 0, Cs = 0;
+  double S = 0, Z = 0, Cs = 0, key = (double)0x7fffffff;
   double m = -INFINITY;
   for (int q = 0; q < r.P; ++q) {
     const double* rec = r.part + ((size_t)b * r.P + q) * kPart;
     S += rec[0];
     Cs += rec[3];
+    key_merge(m, key, rec[1], rec[5]);
     lse_merge(m, Z, rec[1], rec[2], r.T);
   }
   graf_partials g;
@@ -950,6 +1016,8 @@ __global__ void partials_reduce_kernel(ReduceParams r) {
   g.lse_max = m;
   g.lse_sum = Z;
   g.cen_sum = Cs;
+  g.psl_key = key;
+  g.reserved = 0.0;
   r.out[b] = g;
 }
 
@@ -1026,12 +1094,13 @@ struct CombineParams {
 __global__ void combine_partials_kernel(CombineParams c) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= c.B) return;
-  double S = 0, Z = 0, Cs = 0;
+  double S = 0, Z = 0, Cs = 0, key = (double)0x7fffffff;
   double m = -INFINITY;
   for (int q = 0; q < c.G; ++q) {
     const graf_partials g = c.shards[(size_t)q * c.B + b];
     S += g.isl_sum;
     Cs += g.cen_sum;
+    key_merge(m, key, g.lse_max, g.psl_key);
     lse_merge(m, Z, g.lse_max, g.lse_sum, c.T);
   }
   graf_partials o;
@@ -1039,7 +1108,280 @@ __global__ void combine_partials_kernel(CombineParams c) {
   o.lse_max = m;
   o.lse_sum = Z;
   o.cen_sum = Cs;
+  o.psl_key = key;
+  o.reserved = 0.0;
   c.out[b] = o;
+}
+
+// ---------------------------------------------------------------------------
+// Hard PSL (Eq. 19; the section-7 loss L416): loss += lambda * x*
+// and its argmax subgradient, from the combined partials (lse_max = x*, psl_key =
+// the argmax cell).  One CTA per waveform, O(N):
+//   A* = sum_n s[n] conj(s[n-k*]) W^{m* n}        (the one cell, double accumulation)
+//   G  = lambda A*/E^2 (normalized) | lambda A*   (d x*/dA*)
+//   g[p] += H[p] s[p-k*] + conj(H[p+k*]) s[p+k*],  H[n] = G W^{-m* n}
+//   normalized: g -= (2 lambda / E^3) chi* s.
+// Only shard 0 adds the gradient term (the sum over shards is the full gradient);
+// every shard adds the loss (x* is global).
+// ---------------------------------------------------------------------------
+struct PslParams {
+  const float2* s;
+  const graf_partials* stats;
+  int N, M, key_lo, periodic, normalize;
+  float lam;
+  int add_grad;       // 0: this shard does not hold the term
+  int accumulate;     // 1: add into loss/grad (a finalize wrote them), 0: overwrite
+  double* loss;       // nullable
+  float2* grad;
+};
+
+__global__ void __launch_bounds__(256) psl_grad_kernel(PslParams q) {
+  const int b = blockIdx.x;
+  const int N = q.N, M = q.M;
+  const float2* sg = q.s + (size_t)b * N;
+  const graf_partials st = q.stats[b];
+  const long long key = (long long)st.psl_key;
+  const int k = (int)(key / M) + q.key_lo, m = (int)(key % M);
+  const int stride = kMaxM / M;
+  __shared__ double red[2 * 32 + 2];
+  // A* = sum_n s[n] conj(s[n-k]) W^{m n}
+  double ax = 0.0, ay = 0.0;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    int j = n - k;
+    bool ok = true;
+    if (q.periodic) j = ((j % N) + N) % N;
+    else ok = (j >= 0 && j < N);
+    if (ok) {
+      const float2 r = cmulc(sg[n], sg[j]);
+      const float2 w = g_tw[(int)(((long long)m * n) & (M - 1)) * stride];
+      ax += (double)r.x * w.x - (double)r.y * w.y;
+      ay += (double)r.x * w.y + (double)r.y * w.x;
+    }
+  }
+  ax = block_sum<256>(ax, red);
+  ay = block_sum<256>(ay, red);
+  double E = 0.0;
+  if (threadIdx.x < 32) {
+    const double e = warp_energy(sg, N, threadIdx.x);
+    if (threadIdx.x == 0) E = e;
+  }
+  if (threadIdx.x == 0) {
+    red[64] = ax;
+    red[65] = ay;
+    red[0] = E;
+    if (q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)q.lam * st.lse_max;
+  }
+  __syncthreads();
+  const double Ax = red[64], Ay = red[65], Ed = red[0];
+  const double sc = q.normalize ? (double)q.lam / (Ed * Ed) : (double)q.lam;
+  const float2 G = make_float2((float)(sc * Ax), (float)(sc * Ay));
+  const float coef = q.normalize ? (float)(2.0 * q.lam * (Ax * Ax + Ay * Ay) / (Ed * Ed * Ed)) : 0.f;
+  for (int p = threadIdx.x; p < N; p += blockDim.x) {
+    float2 acc = make_float2(0.f, 0.f);
+    if (q.add_grad) {
+      // term 1 (n = p): H[p] s[p-k]
+      int j = p - k;
+      bool ok = true;
+      if (q.periodic) j = ((j % N) + N) % N;
+      else ok = (j >= 0 && j < N);
+      if (ok) {
+        const float2 w = cconj(g_tw[(int)(((long long)m * p) & (M - 1)) * stride]);   // W^{-m p}
+        acc = cadd(acc, cmul(cmul(G, w), sg[j]));
+      }
+      // term 2 (n = p + k): conj(H[p+k]) s[p+k]
+      int n = p + k;
+      ok = true;
+      if (q.periodic) n = ((n % N) + N) % N;
+      else ok = (n >= 0 && n < N);
+      if (ok) {
+        const float2 w = cconj(g_tw[(int)(((long long)m * n) & (M - 1)) * stride]);
+        acc = cadd(acc, cmul(cconj(cmul(G, w)), sg[n]));
+      }
+      const float2 sp = sg[p];
+      acc = make_float2(acc.x - coef * sp.x, acc.y - coef * sp.y);
+    }
+    float2* gp = q.grad + (size_t)b * N + p;
+    *gp = q.accumulate ? cadd(*gp, acc) : acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Spectral variance (the section-7 LPI term; reading R22):
+//   S = DFT_N(s), p = |S|^2 / P, SV = sum (p - mean p)^2 / (N - 1)
+//   dSV/dS* = (c - sum c p) S / P, c = 2 (p - mean p) / (N - 1);  g = DFT^H (dSV/dS*)
+// N <= 1024: the DFT as its sum (one CTA per waveform, a thread per bin; the
+// section-7 N = 256 costs microseconds); N >= 2048: the Stockham row FFT.
+// Reductions: fixed-order shared-memory trees (deterministic).
+// ---------------------------------------------------------------------------
+struct SvParams {
+  const float2* s;
+  int N;
+  float weight;
+  const float* weights;   // [B] or NULL (= weight)
+  int accumulate;
+  double* loss;
+  float2* grad;
+};
+
+// sum over the CTA (blockDim.x a power of two <= 1024), result in every thread
+__device__ __forceinline__ double cta_tree_sum(double v, double* buf) {
+  const int t = threadIdx.x;
+  buf[t] = v;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (t < h) buf[t] += buf[t + h];
+    __syncthreads();
+  }
+  const double r = buf[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) sv_direct_kernel(SvParams q) {
+  extern __shared__ float4 smem_raw[];
+  const int N = q.N, b = blockIdx.x, t = threadIdx.x;
+  float2* ss = reinterpret_cast<float2*>(smem_raw);        // s [N], then dS [N]
+  float2* ds = ss + N;
+  double* buf = reinterpret_cast<double*>(ds + N);          // [blockDim]
+  const float2* sg = q.s + (size_t)b * N;
+  for (int i = t; i < N; i += blockDim.x) ss[i] = sg[i];
+  __syncthreads();
+  const int stride = kMaxM / N;
+  // bins j = t (blockDim >= N): S_j = sum_n s_n W^{jn}, double accumulation
+  double Sx = 0.0, Sy = 0.0;
+  if (t < N) {
+    for (int n = 0; n < N; ++n) {
+      const float2 w = g_tw[((t * n) & (N - 1)) * stride];
+      Sx += (double)ss[n].x * w.x - (double)ss[n].y * w.y;
+      Sy += (double)ss[n].x * w.y + (double)ss[n].y * w.x;
+    }
+  }
+  const double pw = Sx * Sx + Sy * Sy;
+  const double P = cta_tree_sum(t < N ? pw : 0.0, buf);
+  const double pe = pw / P;
+  const double mean = cta_tree_sum(t < N ? pe : 0.0, buf) / N;
+  const double d = pe - mean;
+  const double var = cta_tree_sum(t < N ? d * d : 0.0, buf);
+  const double ce = 2.0 * d / (N - 1);
+  const double cp = cta_tree_sum(t < N ? ce * pe : 0.0, buf);
+  const float wb = q.weights ? q.weights[b] : q.weight;
+  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)wb * (var / (N - 1));
+  if (t < N) {
+    const double f = (double)wb * (ce - cp) / P;
+    ds[t] = make_float2((float)(f * Sx), (float)(f * Sy));
+  }
+  __syncthreads();
+  // g_n = sum_j dS_j W^{-jn}
+  if (t < N) {
+    double gx = 0.0, gy = 0.0;
+    for (int j = 0; j < N; ++j) {
+      const float2 w = g_tw[((t * j) & (N - 1)) * stride];   // conj below
+      gx += (double)ds[j].x * w.x + (double)ds[j].y * w.y;
+      gy += (double)ds[j].y * w.x - (double)ds[j].x * w.y;
+    }
+    float2* gp = q.grad + (size_t)b * N + t;
+    const float2 g = make_float2((float)gx, (float)gy);
+    *gp = q.accumulate ? cadd(*gp, g) : g;
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(Cfg<M>::T) sv_fft_kernel(SvParams q) {
+  using C = Cfg<M>;
+  constexpr int E = C::E, T = C::T;
+  constexpr bool SPLIT = C::SPLIT;
+  constexpr int E2 = SPLIT ? E / 2 : E;
+  static_assert(T >= 32, "one full warp at least");
+  extern __shared__ float4 smem_raw[];
+  float2* sh = reinterpret_cast<float2*>(smem_raw);
+  double* buf = reinterpret_cast<double*>(sh + ((C::XS + 1) & ~1));
+  const int b = blockIdx.x, t = threadIdx.x;
+  const float2* sg = q.s + (size_t)b * M;
+  Twiddles<C::MX, E2> tw;
+  tw.init(t);
+  const float2 wt = SPLIT ? g_tw[t * (kMaxM / M)] : make_float2(1.f, 0.f);
+  SlotSync<T, 1> sync{1};
+  auto toff = [](int e) { return SPLIT ? (e < E2 ? 2 * e * T : 2 * (e - E2) * T + 1) : e * T; };
+  const int tb = SPLIT ? 2 * t : t;
+  float2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = sg[tb + toff(e)];
+  row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);      // S[m], m = t + e T
+  double pw = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) pw += (double)v[e].x * v[e].x + (double)v[e].y * v[e].y;
+  const double P = cta_tree_sum(pw, buf);
+  double sp = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) sp += ((double)v[e].x * v[e].x + (double)v[e].y * v[e].y) / P;
+  const double mean = cta_tree_sum(sp, buf) / M;
+  double var = 0.0, cp = 0.0;
+  float c[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const double pe = ((double)v[e].x * v[e].x + (double)v[e].y * v[e].y) / P;
+    const double d = pe - mean;
+    var += d * d;
+    const double ce = 2.0 * d / (M - 1);
+    c[e] = (float)ce;
+    cp += ce * pe;
+  }
+  var = cta_tree_sum(var, buf);
+  cp = cta_tree_sum(cp, buf);
+  const float wb = q.weights ? q.weights[b] : q.weight;
+  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)wb * (var / (M - 1));
+  const float sc = (float)((double)wb / P);
+  const float cpf = (float)cp;
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = cscale(v[e], (c[e] - cpf) * sc);
+  row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);       // g[n] = sum_m dS_m W^{-mn}
+  float2* gg = q.grad + (size_t)b * M;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    float2* gp = gg + tb + toff(e);
+    *gp = q.accumulate ? cadd(*gp, v[e]) : v[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Adam on the phases of s = exp(j theta), one CTA per waveform (the
+// waveform's step counter is read and advanced by its own CTA: graph-replayable)
+// ---------------------------------------------------------------------------
+struct AdamParams {
+  float* theta;
+  float* m;
+  float* v;
+  int* step;
+  const float2* grad;
+  float2* s_out;
+  int N;
+  float lr, beta1, beta2, eps;
+};
+
+__global__ void __launch_bounds__(256) phase_adam_kernel(AdamParams a) {
+  const int b = blockIdx.x;
+  const int t = a.step[b] + 1;
+  const float bc1 = 1.f - powf(a.beta1, (float)t), bc2 = 1.f - powf(a.beta2, (float)t);
+  for (int i = threadIdx.x; i < a.N; i += blockDim.x) {
+    const size_t j = (size_t)b * a.N + i;
+    const float th = a.theta[j];
+    float sn, cs;
+    sincosf(th, &sn, &cs);
+    const float2 g = a.grad[j];
+    // dL/dtheta = -2 Im(s conj(g)), s = (cs, sn)
+    const float d = -2.f * (sn * g.x - cs * g.y);
+    const float mm = a.beta1 * a.m[j] + (1.f - a.beta1) * d;
+    const float vv = a.beta2 * a.v[j] + (1.f - a.beta2) * d * d;
+    a.m[j] = mm;
+    a.v[j] = vv;
+    const float thn = th - a.lr * (mm / bc1) / (sqrtf(vv / bc2) + a.eps);
+    a.theta[j] = thn;
+    float s2, c2;
+    sincosf(thn, &s2, &c2);
+    a.s_out[j] = make_float2(c2, s2);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) a.step[b] = t;
 }
 
 }  // namespace graf

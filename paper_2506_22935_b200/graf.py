@@ -28,7 +28,8 @@ _LAYOUT = {"raw": L.DOPPLER_RAW, "centered": L.DOPPLER_CENTERED, "centred": L.DO
 @dataclass
 class LossSpec:
     """graf_loss_desc (include/graf.h): region |k|<=k_max, |d|<=d_max minus the
-    mainlobe |k|<=ml_k && |d|<=ml_d; L = lambda_isl*ISL + lambda_psl*softPSL."""
+    mainlobe |k|<=ml_k && |d|<=ml_d; L = lambda_isl*ISL + lambda_psl*softPSL + lambda_hpsl*PSL
+    (hard PSL with its argmax subgradient, the paper's section-7 loss)."""
     k_max: int
     d_max: int
     ml_k: int = 0
@@ -37,6 +38,7 @@ class LossSpec:
     lambda_psl: float = 0.0
     temperature: float = 0.01
     normalize: int = 1
+    lambda_hpsl: float = 0.0
     w_k: Optional[torch.Tensor] = None   # device float32 [2N-1], symmetric
     w_d: Optional[torch.Tensor] = None   # device float32 [M], symmetric
 
@@ -47,7 +49,8 @@ class LossSpec:
     def desc(self) -> L.LossDesc:
         return L.LossDesc(int(self.k_max), int(self.d_max), int(self.ml_k), int(self.ml_d),
                           _ptr(self.w_k), _ptr(self.w_d), float(self.lambda_isl),
-                          float(self.lambda_psl), float(self.temperature), int(self.normalize))
+                          float(self.lambda_psl), float(self.temperature), int(self.normalize),
+                          float(self.lambda_hpsl))
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -102,6 +105,7 @@ class Workspace:
 
 
 _ws = Workspace()
+NPART = 6   # doubles per graf_partials record
 
 
 def _surface_alloc(desc: L.AfDesc, device) -> Optional[torch.Tensor]:
@@ -116,14 +120,14 @@ def af_forward(s: torch.Tensor, M: int, *, out: Optional[str] = "c64", layout: s
                k_begin: Optional[int] = None, k_end: Optional[int] = None, normalize_output: bool = False,
                loss: Optional[LossSpec] = None, shard=(0, 1), ws: Optional[Workspace] = None,
                surface: Optional[torch.Tensor] = None, stream=None, periodic: bool = False):
-    """graf_af_forward: surface window and/or this shard's loss partials [B,4] (float64).
+    """graf_af_forward: surface window and/or this shard's loss partials [B,6] (float64).
     periodic=True: the paper's circular surface (Eq. 2 / Alg. 1), M == N."""
     s = _check_s(s)
     d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic)
     ld = loss.desc() if loss is not None else None
     if surface is None:
         surface = _surface_alloc(d, s.device)
-    partials = torch.empty((s.shape[0], 4), dtype=torch.float64, device=s.device) if loss is not None else None
+    partials = torch.empty((s.shape[0], NPART), dtype=torch.float64, device=s.device) if loss is not None else None
     nbytes = workspace_bytes(d, ld)
     wp, wn = (ws or _ws).get(nbytes, s.device)
     L.check(L.lib().graf_af_forward(ctypes.byref(d), ctypes.byref(ld) if ld else None,
@@ -150,7 +154,7 @@ def af_loss_grad(s: torch.Tensor, M: int, loss: LossSpec, *, global_partials: Op
     if surface is None:
         surface = _surface_alloc(d, s.device)
     if global_partials is not None:
-        assert global_partials.dtype == torch.float64 and global_partials.shape == (B, 4)
+        assert global_partials.dtype == torch.float64 and global_partials.shape == (B, NPART)
     nbytes = workspace_bytes(d, ld)
     wp, wn = (ws or _ws).get(nbytes, s.device)
     L.check(L.lib().graf_af_loss_grad(ctypes.byref(d), ctypes.byref(ld), ctypes.c_void_p(s.data_ptr()),
@@ -181,11 +185,11 @@ def af_backward(s: torch.Tensor, M: int, dA: torch.Tensor, *, k_begin=None, k_en
 
 
 def combine_partials(loss: LossSpec, shards: torch.Tensor, stream=None) -> torch.Tensor:
-    """graf_combine_partials: shards [G,B,4] float64 -> [B,4], in shard order."""
-    G, B, four = shards.shape
-    assert four == 4 and shards.dtype == torch.float64
+    """graf_combine_partials: shards [G,B,6] float64 -> [B,6], in shard order."""
+    G, B, npart = shards.shape
+    assert npart == NPART and shards.dtype == torch.float64
     shards = shards.contiguous()
-    out = torch.empty((B, 4), dtype=torch.float64, device=shards.device)
+    out = torch.empty((B, NPART), dtype=torch.float64, device=shards.device)
     ld = loss.desc()
     if shards.is_cuda:
         L.check(L.lib().graf_combine_partials(ctypes.byref(ld), ctypes.c_void_p(shards.data_ptr()), G, B,
@@ -245,3 +249,90 @@ def af(s, M, layout="centered", k_begin=None, k_end=None, periodic=False):
 
 def af_loss(s, M, spec: LossSpec, periodic=False):
     return AFLoss.apply(s, M, spec, periodic)
+
+
+# ---------------------------------------------------------------------------
+# The paper's section-7 workload:
+# L_b = PSL_b + lambda_b * alpha * SV_b on s = exp(j theta), Adam on theta.
+# Every step is one of the library's kernels (hard-PSL pass, psl_grad, spectral
+# variance, Adam); Python only marshals pointers and replays CUDA graphs.
+# ---------------------------------------------------------------------------
+def spectral_variance(s: torch.Tensor, weight: float = 1.0, weights: Optional[torch.Tensor] = None,
+                      loss: Optional[torch.Tensor] = None, grad: Optional[torch.Tensor] = None,
+                      accumulate: bool = False, stream=None):
+    """graf_spectral_variance -> (weight*SV [B] float64, weight*dSV/ds* [B,N] complex64)."""
+    s = _check_s(s)
+    B, N = s.shape
+    if loss is None:
+        loss = torch.zeros((B,), dtype=torch.float64, device=s.device)
+    if grad is None:
+        grad = torch.zeros((B, N), dtype=torch.complex64, device=s.device)
+    if weights is not None:
+        assert weights.dtype == torch.float32 and weights.is_cuda and weights.shape == (B,)
+    L.check(L.lib().graf_spectral_variance(B, N, ctypes.c_void_p(s.data_ptr()), float(weight), _ptr(weights),
+                                           _ptr(loss), ctypes.c_void_p(grad.data_ptr()), int(bool(accumulate)),
+                                           _stream(stream)))
+    return loss, grad
+
+
+def phase_adam_step(theta, m, v, step, grad, s_out, lr=0.01, betas=(0.9, 0.999), eps=1e-8, stream=None):
+    """graf_phase_adam_step: in place on theta/m/v/step [B,N] float32 / [B] int32; s_out = exp(j theta)."""
+    B, N = theta.shape
+    L.check(L.lib().graf_phase_adam_step(B, N, _ptr(theta), _ptr(m), _ptr(v), _ptr(step), _ptr(grad), _ptr(s_out),
+                                         float(lr), float(betas[0]), float(betas[1]), float(eps), _stream(stream)))
+
+
+class LpiOptimizer:
+    """Batched section-7 optimisation: each waveform b has its own trade-off lambda_b
+    (a lambda sweep x seeds is one batch).  One iteration = hard-PSL pass 1 +
+    argmax subgradient + spectral variance (accumulated) + Adam, captured once as
+    a CUDA graph of `per_graph` iterations and replayed."""
+
+    def __init__(self, theta0: torch.Tensor, lam, spec: Optional[LossSpec] = None, alpha: float = 2000.0,
+                 lr: float = 0.01, periodic: bool = True, per_graph: int = 50):
+        self.theta = theta0.detach().to(torch.float32).contiguous().clone()
+        B, N = self.theta.shape
+        dev = self.theta.device
+        self.spec = spec or LossSpec(k_max=N, d_max=N, lambda_isl=0.0, lambda_psl=0.0, normalize=1)
+        self.spec.lambda_hpsl = 1.0
+        self.spec.lambda_isl = 0.0
+        self.spec.lambda_psl = 0.0
+        lam = torch.as_tensor(lam, dtype=torch.float32, device=dev).expand(B).contiguous()
+        self.weights = (lam * float(alpha)).contiguous()
+        self.lr, self.periodic = lr, periodic
+        self.m = torch.zeros_like(self.theta)
+        self.v = torch.zeros_like(self.theta)
+        self.step = torch.zeros((B,), dtype=torch.int32, device=dev)
+        self.s = torch.polar(torch.ones_like(self.theta), self.theta).to(torch.complex64).contiguous()
+        self.grad = torch.empty((B, N), dtype=torch.complex64, device=dev)
+        self.loss = torch.empty((B,), dtype=torch.float64, device=dev)
+        self.ws = Workspace()
+        self.stream = torch.cuda.Stream(dev)
+        self.per_graph = per_graph
+        self.graph = None
+
+    def _iteration(self):
+        B, N = self.theta.shape
+        af_loss_grad(self.s, N, self.spec, ws=self.ws, grad=self.grad, loss_out=self.loss, stream=self.stream,
+                     periodic=self.periodic)
+        spectral_variance(self.s, weights=self.weights, loss=self.loss, grad=self.grad, accumulate=True,
+                          stream=self.stream)
+        phase_adam_step(self.theta, self.m, self.v, self.step, self.grad, self.s, lr=self.lr, stream=self.stream)
+
+    def run(self, iters: int) -> torch.Tensor:
+        """Advance `iters` iterations; returns the loss [B] of the last one (float64)."""
+        with torch.cuda.stream(self.stream):
+            if self.graph is None:
+                self._iteration()                              # workspace + twiddles, outside capture
+                iters -= 1
+                self.graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph, stream=self.stream):
+                    for _ in range(self.per_graph):
+                        self._iteration()
+            while iters >= self.per_graph:
+                self.graph.replay()
+                iters -= self.per_graph
+            for _ in range(iters):
+                self._iteration()
+        self.stream.synchronize()
+        return self.loss

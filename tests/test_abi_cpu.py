@@ -101,11 +101,12 @@ def test_host_combine_partials_is_exact_lse_merge():
     import math
     lib = L.lib()
     T = 0.5
-    ld = L.LossDesc(1, 1, 0, 0, None, None, 1.0, 1.0, T, 1)
+    ld = L.LossDesc(1, 1, 0, 0, None, None, 1.0, 1.0, T, 1, 0.0)
     # two shards, one waveform: shard sums of exp((x-m)/T) over {0.1, 0.3} and {0.7}
-    sh = (L.Partials * 2)(L.Partials(1.0, 0.3, math.exp((0.1 - 0.3) / T) + 1.0, 0.0),
-                          L.Partials(2.0, 0.7, 1.0, 0.0))
+    sh = (L.Partials * 2)(L.Partials(1.0, 0.3, math.exp((0.1 - 0.3) / T) + 1.0, 0.0, 7.0, 0.0),
+                          L.Partials(2.0, 0.7, 1.0, 0.0, 5.0, 0.0))
     out = L.Partials()
     assert lib.graf_combine_partials(ctypes.byref(ld), sh, 2, 1, ctypes.byref(out), 0, None) == L.GRAF_OK
     ref = sum(math.exp((x - 0.7) / T) for x in (0.1, 0.3, 0.7))
     assert out.isl_sum == 3.0 and abs(out.lse_max - 0.7) < 1e-7 and abs(out.lse_sum - ref) < 1e-6
+    assert out.psl_key == 5.0                      # the argmax cell of the larger max

@@ -49,7 +49,7 @@ class OracleShardBackend:
                 Z = float(np.sum(np.exp((x[mask] - c) / spec.temperature)))
             else:
                 c, Z = -np.inf, 0.0
-            out.append([S, c, Z, 0.0])
+            out.append([S, c, Z, 0.0, 0.0, 0.0])
         return torch.tensor(out, dtype=torch.float64)
 
     def combine(self, spec, parts):
