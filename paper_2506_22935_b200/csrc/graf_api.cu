@@ -325,7 +325,7 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   if (occ < 1) return cudaErrorInvalidConfiguration;
   size_t smem = pl.smem;
   rp.gpad = 0;
-  if (pl.gpad_ok && KIND != K_ADJ && KIND != K_FWD) {
+  if (pl.gpad_ok && KIND != K_ADJ && KIND != K_FWD && KIND != K_FWDA) {
     if (pl.gpad_mode < 0) {
       int occ_g = 0;
       const bool fits = pl.smem + pl.smem_gpad <= 227 * 1024;
@@ -403,7 +403,10 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
 template <int M>
 cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind, bool wgt) {
   switch (kind) {
-    case K_FWD: return wgt ? launch_kernel<M, K_FWD, true>(pl, rp, B, st) : launch_kernel<M, K_FWD, false>(pl, rp, B, st);
+    case K_FWD:
+      if (rp.want_argmax)
+        return wgt ? launch_kernel<M, K_FWDA, true>(pl, rp, B, st) : launch_kernel<M, K_FWDA, false>(pl, rp, B, st);
+      return wgt ? launch_kernel<M, K_FWD, true>(pl, rp, B, st) : launch_kernel<M, K_FWD, false>(pl, rp, B, st);
     case K_ISL: return wgt ? launch_kernel<M, K_ISL, true>(pl, rp, B, st) : launch_kernel<M, K_ISL, false>(pl, rp, B, st);
     case K_PASS2:
       return wgt ? launch_kernel<M, K_PASS2, true>(pl, rp, B, st) : launch_kernel<M, K_PASS2, false>(pl, rp, B, st);
@@ -577,7 +580,7 @@ graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L,
   r.T = L->lambda_psl != 0.f ? L->temperature : 1.f;
   r.invT = 1.f / r.T;
   r.out = out;
-  partials_reduce_kernel<<<(r.B + 127) / 128, 128, 0, st>>>(r);
+  partials_reduce_kernel<<<(r.B + 3) / 4, 128, 0, st>>>(r);   // a warp per waveform
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++t_launches;
   return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "partials_reduce_kernel launch");
@@ -837,11 +840,12 @@ graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, floa
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   SvParams q{static_cast<const float2*>(s), n, weight, weights, accumulate ? 1 : 0, loss,
              static_cast<float2*>(grad)};
-  if (n <= 1024) {
-    const int threads = std::max(32, n);
+  if (n <= 32) {
+    const int threads = 32;
     const size_t smem = sizeof(float2) * 2 * (size_t)n + sizeof(double) * threads;
     sv_direct_kernel<<<(unsigned)batch, threads, smem, cs>>>(q);
   } else {
+    // Stockham FFT with T = N/E >= 32 threads (E = N/32 up to 16)
     auto go = [&](auto kern, int T, int XS) -> cudaError_t {
       const size_t smem = sizeof(float2) * (size_t)((XS + 1) & ~1) + sizeof(double) * T;
       cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -849,12 +853,19 @@ graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, floa
       kern<<<(unsigned)batch, T, smem, cs>>>(q);
       return cudaSuccess;
     };
+#define GRAF_SV(M_, E_) go(sv_fft_kernel<M_, E_>, SvCfg<M_, E_>::T, SvCfg<M_, E_>::XS)
     switch (n) {
-      case 2048: e = go(sv_fft_kernel<2048>, Cfg<2048>::T, Cfg<2048>::XS); break;
-      case 4096: e = go(sv_fft_kernel<4096>, Cfg<4096>::T, Cfg<4096>::XS); break;
-      case 8192: e = go(sv_fft_kernel<8192>, Cfg<8192>::T, Cfg<8192>::XS); break;
-      default: e = go(sv_fft_kernel<16384>, Cfg<16384>::T, Cfg<16384>::XS); break;
+      case 64: e = GRAF_SV(64, 2); break;
+      case 128: e = GRAF_SV(128, 4); break;
+      case 256: e = GRAF_SV(256, 8); break;
+      case 512: e = GRAF_SV(512, 16); break;
+      case 1024: e = GRAF_SV(1024, 16); break;
+      case 2048: e = GRAF_SV(2048, 16); break;
+      case 4096: e = GRAF_SV(4096, 16); break;
+      case 8192: e = GRAF_SV(8192, 16); break;
+      default: e = GRAF_SV(16384, 16); break;
     }
+#undef GRAF_SV
     if (e != cudaSuccess) return cuda_fail(e, "sv_fft_kernel attribute");
   }
   e = cudaGetLastError();

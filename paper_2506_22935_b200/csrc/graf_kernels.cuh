@@ -16,6 +16,8 @@
 //   K_ISL   a0-a7 in ONE pass      (ISL-only losses: f' = lambda_isl*w is known up front)
 //   K_PASS2 a0-a7 with f' from the combined pass-1 partials (soft-PSL)
 //   K_ADJ   dA row -> a6-a7        (graf_af_backward, unfolded rows)
+//   K_FWDA  K_FWD that also tracks the hard-PSL argmax cell (its own instantiation,
+//           so the plain forward pass carries none of that code)
 // Rows are folded to k >= 0 (symmetric masks/weights): row k > 0 stands for
 // rows +k and -k (loss sums and gradient terms counted twice; SURVEY §8(c)
 // "symmetric-loss identities").
@@ -27,7 +29,7 @@
 
 namespace graf {
 
-enum : int { K_FWD = 0, K_ISL = 1, K_PASS2 = 2, K_ADJ = 3 };
+enum : int { K_FWD = 0, K_ISL = 1, K_PASS2 = 2, K_ADJ = 3, K_FWDA = 4 };   // K_FWDA: K_FWD + hard-PSL argmax
 constexpr int kPart = 8;  // doubles per CTA partial record: S, max, Z, C, fchi, -, -, -
 
 struct RowParams {
@@ -307,7 +309,7 @@ struct MinBlocks {
 #ifdef GRAF_MINB
   static constexpr int value = GRAF_MINB;
 #else
-  static constexpr int value = M <= 16 ? 2 : M == 1024 ? (KIND == 0 ? 3 : 2) : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
+  static constexpr int value = M <= 16 ? 2 : M == 1024 ? ((KIND == 0 || KIND == 4) ? 3 : 2) : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
 #endif
 };
 // radix-2 split stage between the two M/2-point halves (twiddle W_M^{t + e T} =
@@ -432,7 +434,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   using C = Cfg<M>;
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
   constexpr int LT = ilog2(T);
-  constexpr bool GRAD = (KIND != K_FWD);
+  constexpr bool FWD = (KIND == K_FWD || KIND == K_FWDA);
+  constexpr bool GRAD = !FWD;
   constexpr bool SPLIT = C::SPLIT;
   constexpr int E2 = SPLIT ? E / 2 : E;
   extern __shared__ float4 smem_raw[];
@@ -516,7 +519,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   bool use_centred = false;
   if constexpr (KIND == K_PASS2) {
     const graf_partials g = p.stats[b];
-    lse = (float)(g.lse_max + (double)p.T * log(g.lse_sum));
+    // without a soft-PSL term the exp factor must vanish, not become 0 * inf
+    lse = p.lam_psl != 0.f ? (float)(g.lse_max + (double)p.T * log(g.lse_sum)) : INFINITY;
     if (p.centred) {
       const double zc = p.omega + g.cen_sum;
       use_centred = isfinite(zc) && (g.lse_max - p.xbar) * p.invT <= 40.0;
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       invZc = (float)(1.0 / zc);
     }
   }
-  const bool want_lse = (KIND == K_FWD) && p.loss_on && p.lam_psl != 0.f;
+  const bool want_lse = FWD && p.loss_on && p.lam_psl != 0.f;
 
   SlotSync<T, S> sync{1 + slot};
   float2* sh = xch + (size_t)slot * XS;
@@ -720,10 +724,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
           const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
           rowS = fmaf(in ? w : 0.f, chi, rowS);
-          if constexpr (KIND == K_FWD) {
+          if constexpr (FWD) {
             const float x = p.normalize ? chi * invE2 : chi;
             rowM = fmaxf(rowM, in ? x : -INFINITY);
-            if (p.want_argmax) {
+            if constexpr (KIND == K_FWDA) {
               // canonical (row-major first) cell of the mirrored pair holding this value
               const int m = t + e * T;
               const int mm = (M - m) & (M - 1);
@@ -741,8 +745,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             if (use_centred) {
               fp = p.lam_psl * (expm1_fast((x - p.xbar) * p.invT) - ebar) * invZc;
             } else {
-              fp = p.lam_isl * w;
-              if (p.lam_psl != 0.f) fp += p.lam_psl * exp_fast((x - lse) * p.invT);
+              fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
             }
             fp = in ? fp : 0.f;
             rowF = fmaf(fp, chi, rowF);
@@ -752,7 +755,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         if constexpr (KIND == K_ISL) rowF = p.lam_isl * rowS;
         accS += (double)(mult * rowS);
         accF += (double)(mult * rowF);
-        if constexpr (KIND == K_FWD) {
+        if constexpr (FWD) {
           if (want_lse && rowM > -INFINITY) {
             if (rowM > accM) {
               accZ = (accM == -INFINITY) ? 0.0 : accZ * (double)exp_fast((accM - rowM) * p.invT);
@@ -894,7 +897,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     const double F0 = block_sum<THREADS>(accF, scratch);
     double Z0 = 0.0, C0 = 0.0;
     float M0 = -INFINITY;
-    if constexpr (KIND == K_FWD) {
+    if constexpr (FWD) {
       M0 = block_max_all<THREADS>(accM, scratch);
       if (want_lse) {
         const double zs = (accM == -INFINITY) ? 0.0 : accZ * (double)exp_fast((accM - M0) * p.invT);
@@ -903,9 +906,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       }
     }
     int K0 = 0x7fffffff;
-    if constexpr (KIND == K_FWD) {
-      if (p.want_argmax) K0 = block_argmax_key<THREADS>(argX, argK, scratch);
-    }
+    if constexpr (KIND == K_FWDA) K0 = block_argmax_key<THREADS>(argX, argK, scratch);
     if (threadIdx.x == 0) {
       rec[0] = S0;
       rec[1] = (double)M0;
@@ -999,26 +1000,43 @@ struct ReduceParams {
   graf_partials* out;
 };
 
+// one warp per waveform: lane l merges records l, l+32, ... in order, then a fixed
+// shuffle-down tree merges the lanes (deterministic)
+__device__ __forceinline__ void merge_rec(double& S, double& m, double& Z, double& Cs, double& key, double S2,
+                                          double m2, double Z2, double C2, double key2, float T) {
+  S += S2;
+  Cs += C2;
+  key_merge(m, key, m2, key2);
+  lse_merge(m, Z, m2, Z2, T);
+}
+
 __global__ void partials_reduce_kernel(ReduceParams r) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= r.B) return;
+  const int b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= r.B) return;   // warp-uniform
   double S = 0, Z = 0, Cs = 0, key = (double)0x7fffffff;
   double m = -INFINITY;
-  for (int q = 0; q < r.P; ++q) {
+  for (int q = lane; q < r.P; q += 32) {
     const double* rec = r.part + ((size_t)b * r.P + q) * kPart;
-    S += rec[0];
-    Cs += rec[3];
-    key_merge(m, key, rec[1], rec[5]);
-    lse_merge(m, Z, rec[1], rec[2], r.T);
+    merge_rec(S, m, Z, Cs, key, rec[0], rec[1], rec[2], rec[3], rec[5], r.T);
   }
-  graf_partials g;
-  g.isl_sum = S;
-  g.lse_max = m;
-  g.lse_sum = Z;
-  g.cen_sum = Cs;
-  g.psl_key = key;
-  g.reserved = 0.0;
-  r.out[b] = g;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double S2 = __shfl_down_sync(0xffffffffu, S, off), m2 = __shfl_down_sync(0xffffffffu, m, off);
+    const double Z2 = __shfl_down_sync(0xffffffffu, Z, off), C2 = __shfl_down_sync(0xffffffffu, Cs, off);
+    const double k2 = __shfl_down_sync(0xffffffffu, key, off);
+    if (lane + off < 32) merge_rec(S, m, Z, Cs, key, S2, m2, Z2, C2, k2, r.T);
+  }
+  if (lane == 0) {
+    graf_partials g;
+    g.isl_sum = S;
+    g.lse_max = m;
+    g.lse_sum = Z;
+    g.cen_sum = Cs;
+    g.psl_key = key;
+    g.reserved = 0.0;
+    r.out[b] = g;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1247,14 +1265,24 @@ __global__ void __launch_bounds__(1024) sv_direct_kernel(SvParams q) {
   for (int i = t; i < N; i += blockDim.x) ss[i] = sg[i];
   __syncthreads();
   const int stride = kMaxM / N;
-  // bins j = t (blockDim >= N): S_j = sum_n s_n W^{jn}, double accumulation
+  // bins j = t (blockDim >= N): S_j = sum_n s_n W^{jn} (fp32 FMA chains, 4 partial
+  // sums for ILP; N <= 1024 terms keep the relative error ~1e-6)
   double Sx = 0.0, Sy = 0.0;
   if (t < N) {
-    for (int n = 0; n < N; ++n) {
-      const float2 w = g_tw[((t * n) & (N - 1)) * stride];
-      Sx += (double)ss[n].x * w.x - (double)ss[n].y * w.y;
-      Sy += (double)ss[n].x * w.y + (double)ss[n].y * w.x;
+    float ax[4] = {0.f, 0.f, 0.f, 0.f}, ay[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int n = 0; n < N; n += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (n + u < N) {
+          const float2 w = g_tw[((t * (n + u)) & (N - 1)) * stride];
+          const float2 x = ss[n + u];
+          ax[u] = fmaf(x.x, w.x, fmaf(-x.y, w.y, ax[u]));
+          ay[u] = fmaf(x.x, w.y, fmaf(x.y, w.x, ay[u]));
+        }
+      }
     }
+    Sx = (double)((ax[0] + ax[1]) + (ax[2] + ax[3]));
+    Sy = (double)((ay[0] + ay[1]) + (ay[2] + ay[3]));
   }
   const double pw = Sx * Sx + Sy * Sy;
   const double P = cta_tree_sum(t < N ? pw : 0.0, buf);
@@ -1273,33 +1301,45 @@ __global__ void __launch_bounds__(1024) sv_direct_kernel(SvParams q) {
   __syncthreads();
   // g_n = sum_j dS_j W^{-jn}
   if (t < N) {
-    double gx = 0.0, gy = 0.0;
-    for (int j = 0; j < N; ++j) {
-      const float2 w = g_tw[((t * j) & (N - 1)) * stride];   // conj below
-      gx += (double)ds[j].x * w.x + (double)ds[j].y * w.y;
-      gy += (double)ds[j].y * w.x - (double)ds[j].x * w.y;
+    float gx[4] = {0.f, 0.f, 0.f, 0.f}, gy[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < N; j += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j + u < N) {
+          const float2 w = g_tw[((t * (j + u)) & (N - 1)) * stride];   // conj below
+          const float2 x = ds[j + u];
+          gx[u] = fmaf(x.x, w.x, fmaf(x.y, w.y, gx[u]));
+          gy[u] = fmaf(x.y, w.x, fmaf(-x.x, w.y, gy[u]));
+        }
+      }
     }
     float2* gp = q.grad + (size_t)b * N + t;
-    const float2 g = make_float2((float)gx, (float)gy);
+    const float2 g = make_float2((gx[0] + gx[1]) + (gx[2] + gx[3]), (gy[0] + gy[1]) + (gy[2] + gy[3]));
     *gp = q.accumulate ? cadd(*gp, g) : g;
   }
 }
 
-template <int M>
-__global__ void __launch_bounds__(Cfg<M>::T) sv_fft_kernel(SvParams q) {
-  using C = Cfg<M>;
-  constexpr int E = C::E, T = C::T;
-  constexpr bool SPLIT = C::SPLIT;
-  constexpr int E2 = SPLIT ? E / 2 : E;
+// the spectral-variance FFT: one row slot of T = M/E >= 32 threads per waveform
+template <int M, int E>
+struct SvCfg {
+  static constexpr int T = M / E;
+  static constexpr int XS = M + M / Pad<E>::P;
   static_assert(T >= 32, "one full warp at least");
+};
+
+template <int M, int E>
+__global__ void __launch_bounds__(M / E) sv_fft_kernel(SvParams q) {
+  constexpr int T = SvCfg<M, E>::T;
+  constexpr bool SPLIT = false;
+  constexpr int E2 = E;
   extern __shared__ float4 smem_raw[];
   float2* sh = reinterpret_cast<float2*>(smem_raw);
-  double* buf = reinterpret_cast<double*>(sh + ((C::XS + 1) & ~1));
+  double* buf = reinterpret_cast<double*>(sh + ((SvCfg<M, E>::XS + 1) & ~1));
   const int b = blockIdx.x, t = threadIdx.x;
   const float2* sg = q.s + (size_t)b * M;
-  Twiddles<C::MX, E2> tw;
+  Twiddles<M, E2> tw;
   tw.init(t);
-  const float2 wt = SPLIT ? g_tw[t * (kMaxM / M)] : make_float2(1.f, 0.f);
+  const float2 wt = make_float2(1.f, 0.f);
   SlotSync<T, 1> sync{1};
   auto toff = [](int e) { return SPLIT ? (e < E2 ? 2 * e * T : 2 * (e - E2) * T + 1) : e * T; };
   const int tb = SPLIT ? 2 * t : t;

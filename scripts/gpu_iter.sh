@@ -12,3 +12,5 @@ timeout 600 python bench.py --config 3 --mode forward --steps 10 --warmup 3 --no
 python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c3fwd.json')); r=d['roofline']; print('c3fwd', d['ms_per_step'], r['bound'], r['frac'])"
 timeout 600 python bench.py --config 2 --periodic --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c2per.json 2> gpurun_out/bench_${TAG}_c2per.err
 python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c2per.json')); r=d['roofline']; print('c2per', d['ms_per_step'], r['bound'], r['frac'])"
+timeout 600 python bench.py --mode lpi --steps 10 --warmup 3 > gpurun_out/bench_${TAG}_lpi.json 2> gpurun_out/bench_${TAG}_lpi.err
+python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_lpi.json')); print('lpi it/s', d['value'], 'full2000 ms', d['config']['full_2000_iterations_ms'], 'loss', d['config']['final_loss_median'])"

@@ -90,7 +90,7 @@ def test_hard_psl_sharding_algebra():
         assert (gsum - g1).abs().max().item() <= 1e-4 * g1.abs().max().item()
 
 
-@pytest.mark.parametrize("N", [2, 8, 64, 256, 1024, 2048, 4096])
+@pytest.mark.parametrize("N", [2, 8, 32, 64, 128, 256, 512, 1024, 2048, 4096])
 def test_spectral_variance(N):
     s = cg(3, N, N + 1)
     w = torch.tensor([1.0, 0.5, 3.0], dtype=torch.float32, device="cuda")
