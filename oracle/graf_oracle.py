@@ -53,7 +53,7 @@ __all__ = [
     "lag_products", "ambiguity", "region", "loss_terms", "loss",
     "loss_and_grad", "adjoint", "correlate", "surface", "loss_and_grad_chunked",
     "periodic_ambiguity", "hard_psl_and_grad", "spectral_variance_and_grad", "phase_grad",
-    "adam_step", "lpi_loss_and_grad",
+    "adam_step", "lpi_loss_and_grad", "match_loss_and_grad",
 ]
 
 
@@ -440,3 +440,35 @@ def lpi_loss_and_grad(theta: np.ndarray, spec: LossSpec, lam: float, alpha: floa
     sv, gs = spectral_variance_and_grad(s)
     L = psl + lam * alpha * sv
     return L, phase_grad(s, gp + lam * alpha * gs), dict(psl=psl, sv=sv)
+
+
+# ---------------------------------------------------------------------------
+# Match loss: L_match = ||x - x_target||_F^2 over the
+# sidelobe region Omega_s (reading R24: the same region as ISL/PSL; x = chi/E^2
+# normalized | chi raw), the target laid out like the surface window
+# (rows k_begin..k_end-1, Doppler raw or centred).
+# ---------------------------------------------------------------------------
+def match_loss_and_grad(s: np.ndarray, M: int, spec: LossSpec, target: np.ndarray, k_begin: int,
+                        layout: str = "centered", periodic: bool = False):
+    """(L_match, g = dL_match/ds*) with f' = dL/dx = 2 (x - t) on Omega_s."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    rows, bins, mask, _ = region(n, M, spec, periodic)
+    E = energy(s)
+    A = ambiguity(s, M, rows, bins, periodic)
+    chi = A.real ** 2 + A.imag ** 2
+    x = chi / E ** 2 if spec.normalize else chi
+    tgt = np.asarray(target, dtype=np.float64)
+    ri = rows - k_begin
+    if periodic:
+        ri = ri % n if tgt.shape[0] == n else ri
+    ci = (bins + M // 2) % M if layout == "centered" else bins
+    t = tgt[ri[:, None], ci[None, :]]
+    diff = np.where(mask, x - t, 0.0)
+    L = float(np.sum(diff ** 2))
+    fp = 2.0 * diff
+    G = fp * A / E ** 2 if spec.normalize else fp * A
+    g = adjoint(s, M, G, rows, bins, periodic)
+    if spec.normalize:
+        g = g - (2.0 / E ** 3) * float(np.sum(fp * chi)) * s
+    return L, g

@@ -514,3 +514,27 @@ def test_lpi_phase_gradient_central_differences():
     fd = _fd(lambda z: O.lpi_loss_and_grad(z, spec, lam=0.5)[0], th, complex_input=False)
     np.testing.assert_allclose(gth, fd.real, atol=1e-6 * max(1.0, np.abs(fd).max()))
     assert abs(L - (parts["psl"] + 0.5 * 2000.0 * parts["sv"])) < 1e-15 * max(1, L)
+
+
+# ---------------------------------------------------------------- match loss (NEXT-3)
+@pytest.mark.parametrize("periodic,layout", [(False, "centered"), (False, "raw"), (True, "centered")])
+def test_match_loss_pins(periodic, layout):
+    n, M = 8, 8
+    s = rs(n, 120)
+    spec = O.LossSpec(k_max=3, d_max=3, ml_k=0, ml_d=1, normalize=1)
+    kb = 0 if periodic else -(n - 1)
+    rows_w = n if periodic else 2 * n - 1
+    surf = O.surface(s, M, "pow", layout, k_begin=kb, k_end=kb + rows_w, periodic=periodic) / O.energy(s) ** 2
+    # target = the surface itself: zero loss, zero gradient
+    L, g = O.match_loss_and_grad(s, M, spec, surf, kb, layout, periodic)
+    assert L < 1e-28 and np.abs(g).max() < 1e-14
+    # target = 0: L = sum over Omega of x^2 (cell count from the region)
+    L0, _ = O.match_loss_and_grad(s, M, spec, np.zeros_like(surf), kb, layout, periodic)
+    t = O.loss_terms(s, M, spec, periodic)
+    assert abs(L0 - np.sum(t["x"][t["mask"]] ** 2)) < 1e-14 * max(1, L0)
+    # central differences on a random target
+    tgt = SplitMix64(121).uniform(surf.size).reshape(surf.shape) * 0.2
+    L, g = O.match_loss_and_grad(s, M, spec, tgt, kb, layout, periodic)
+    fd = _fd(lambda z: O.match_loss_and_grad(z, M, spec, tgt, kb, layout, periodic)[0], s)
+    np.testing.assert_allclose(2 * g, fd, atol=1e-6 * max(1.0, np.abs(fd).max()))
+    assert abs(np.vdot(g, s).imag) < 1e-10 * max(1, np.abs(g).max())
