@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GRAF_ABI_VERSION 3
+#define GRAF_ABI_VERSION 4
 #define GRAF_MAX_M 16384
 
 typedef enum {
@@ -111,6 +111,12 @@ typedef struct {
                                argmax subgradient (the paper's section-7 loss, L416); ties go to
                                the lowest row-major (delay, raw Doppler bin) cell (reading R23).
                                Needs the global max, so it runs pass 1 like soft-PSL.  (ABI v3) */
+  float lambda_match;       /* weight of the match loss ||x - target||^2 summed over Omega (
+                               reading R24).  Not combinable with soft-PSL (lambda_psl != 0). */
+  const float* target;      /* device fp32 target x_target laid out like the surface window of
+                               graf_af_desc ([k_end - k_begin][M], doppler_layout; periodic: a full
+                               window of N delays); the window must hold every delay of Omega */
+  int64_t target_stride;    /* floats between waveforms' targets (0: one target for the batch) (ABI v4) */
 } graf_loss_desc;
 
 /* Per-waveform partial sums over the rows a call covered (exactly combinable

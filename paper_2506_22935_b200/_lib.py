@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # GRAF_LIB_PATH: tuning builds only (scripts/tune.py); the default is the in-tree library.
 LIB_PATH = os.environ.get("GRAF_LIB_PATH") or os.path.join(PKG, "libgraf.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_ENONFINITE, GRAF_EWORKSPACE = range(6)
 OUT_NONE, OUT_C64, OUT_ABS_F32, OUT_POW_F32 = range(4)
 DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
@@ -32,7 +32,8 @@ class LossDesc(ctypes.Structure):
     _fields_ = [("k_max", c_int32), ("d_max", c_int32), ("ml_k", c_int32), ("ml_d", c_int32),
                 ("w_k", c_void_p), ("w_d", c_void_p),
                 ("lambda_isl", c_float), ("lambda_psl", c_float), ("temperature", c_float),
-                ("normalize", c_int32), ("lambda_hpsl", c_float)]
+                ("normalize", c_int32), ("lambda_hpsl", c_float), ("lambda_match", c_float),
+                ("target", c_void_p), ("target_stride", c_int64)]
 
 
 class Partials(ctypes.Structure):

@@ -167,8 +167,21 @@ graf_status check_loss(const graf_af_desc* af, const graf_loss_desc* L) {
     return fail(GRAF_EINVAL, "negative region bound");
   if (L->normalize != 0 && L->normalize != 1) return fail(GRAF_EINVAL, "normalize must be 0 or 1");
   if (L->lambda_psl != 0.f && !(L->temperature > 0.f)) return fail(GRAF_EINVAL, "temperature must be > 0");
-  if (!std::isfinite(L->lambda_isl) || !std::isfinite(L->lambda_psl) || !std::isfinite(L->lambda_hpsl))
+  if (!std::isfinite(L->lambda_isl) || !std::isfinite(L->lambda_psl) || !std::isfinite(L->lambda_hpsl) ||
+      !std::isfinite(L->lambda_match))
     return fail(GRAF_EINVAL, "non-finite lambda");
+  if (L->lambda_match != 0.f) {
+    if (!L->target || (reinterpret_cast<uintptr_t>(L->target) & 3u)) return fail(GRAF_EINVAL, "match target NULL or misaligned");
+    if (L->lambda_psl != 0.f) return fail(GRAF_EUNSUPPORTED, "match loss with soft-PSL (v1: ISL and hard PSL only)");
+    if (L->target_stride < 0) return fail(GRAF_EINVAL, "negative target_stride");
+    // the target window must hold every delay of the region (R24)
+    const int klm = std::min(L->k_max, af->periodic ? af->n / 2 : af->n - 1);
+    if (af->periodic ? (af->k_end - af->k_begin != af->n) : (af->k_begin > -klm || af->k_end <= klm))
+      return fail(GRAF_EINVAL, "match target window [%d, %d) does not cover the region's delays", af->k_begin,
+                  af->k_end);
+    if (af->k_begin < -(af->n - 1) || af->k_end > af->n || af->k_begin >= af->k_end)
+      return fail(GRAF_EINVAL, "match target window [%d, %d) invalid", af->k_begin, af->k_end);
+  }
   const int kl = std::min(L->k_max, af->periodic ? af->n / 2 : af->n - 1);
   const int dl = std::min(L->d_max, af->m / 2);
   const bool nonempty = kl > L->ml_k || dl > L->ml_d;
@@ -411,6 +424,8 @@ cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st,
     case K_PASS2:
       return wgt ? launch_kernel<M, K_PASS2, true>(pl, rp, B, st) : launch_kernel<M, K_PASS2, false>(pl, rp, B, st);
     case K_ADJ: return launch_kernel<M, K_ADJ, false>(pl, rp, B, st);
+    case K_MATCH:
+      return wgt ? launch_kernel<M, K_MATCH, true>(pl, rp, B, st) : launch_kernel<M, K_MATCH, false>(pl, rp, B, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -460,6 +475,9 @@ void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
   rp.centred = (L->normalize && !L->w_k && !L->w_d && full && L->lambda_psl != 0.f) ? 1 : 0;
   rp.omega = (double)(af->periodic ? N : 2 * N - 1) * M - 1.0;   // |Omega| of the full plane
   rp.want_argmax = L->lambda_hpsl != 0.f ? 1 : 0;
+  rp.lam_match = L->lambda_match;
+  rp.target = L->target;
+  rp.target_stride = L->target_stride;
   rp.key_lo = (af->periodic && 2 * rp.kloss == N) ? -rp.kloss + 1 : -rp.kloss;
   rp.xbar = (float)((M - 1) / rp.omega);
 }
@@ -550,6 +568,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
   f.lam_psl = L ? L->lambda_psl : 0.f;
   f.T = (L && L->lambda_psl != 0.f) ? L->temperature : 1.f;
   f.invT = 1.f / f.T;
+  f.lam_match = L ? L->lambda_match : 0.f;
   f.loss = loss;
   f.grad = static_cast<float2*>(grad);
   const long long B = af->batch;
@@ -710,8 +729,18 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   const graf_partials* stats = global;
   const bool hpsl = loss->lambda_hpsl != 0.f;       // hard PSL (section-7 loss), reading R23
   const bool soft = loss->lambda_psl != 0.f;
-  const bool dense = loss->lambda_isl != 0.f || soft;   // terms with a per-cell f'
-  if (!soft && !hpsl) {
+  const bool match = loss->lambda_match != 0.f;    // match loss, reading R24
+  const bool dense = loss->lambda_isl != 0.f || soft || match;   // terms with a per-cell f'
+  if (match && global) return fail(GRAF_EUNSUPPORTED, "match loss with global partials (v1: unsharded)");
+  if (match && !hpsl) {
+    // one pass: f' = lambda_isl w + lambda_match (2x - t1 - t2) is known per cell
+    if (pl.U > 0) {
+      prof_mark(true, cs);
+      e = launch_rows(pl, rp, (int)af->batch, cs, K_MATCH);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (match) launch");
+      prof_mark(false, cs);
+    }
+  } else if (!soft && !hpsl) {
     // single fused pass (f' = lambda_isl * w known up front); unsharded calls also
     // fuse the finalize into the row kernel when a waveform's CTAs fit one cluster
     pl.fuse_req = (global == nullptr);
@@ -735,7 +764,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     }
     rp.stats = stats;
     if (pl.U > 0 && dense) {
-      e = launch_rows(pl, rp, (int)af->batch, cs, K_PASS2);
+      e = launch_rows(pl, rp, (int)af->batch, cs, match ? K_MATCH : K_PASS2);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 2) launch");
     }
     if (pl.U > 0) prof_mark(false, cs);

@@ -29,7 +29,8 @@
 
 namespace graf {
 
-enum : int { K_FWD = 0, K_ISL = 1, K_PASS2 = 2, K_ADJ = 3, K_FWDA = 4 };   // K_FWDA: K_FWD + hard-PSL argmax
+enum : int { K_FWD = 0, K_ISL = 1, K_PASS2 = 2, K_ADJ = 3, K_FWDA = 4, K_MATCH = 5 };
+// K_FWDA: K_FWD + hard-PSL argmax;  K_MATCH: one pass with f' = lambda_isl w + match term
 constexpr int kPart = 8;  // doubles per CTA partial record: S, max, Z, C, fchi, -, -, -
 
 struct RowParams {
@@ -67,6 +68,10 @@ struct RowParams {
   // (delay index from key_lo) * M + raw Doppler bin, ties -> lowest key (reading R23)
   int want_argmax;
   int key_lo;
+  // match loss (K_MATCH): target laid out like the surface window, per waveform stride
+  float lam_match;
+  const float* target;
+  long long target_stride;
   // fused finalize (K_ISL, P <= 8 CTAs per waveform launched as one thread-block
   // cluster): cluster rank 0 combines the CTAs' partials over distributed shared
   // memory and writes loss and grad directly (no partial records, no finalize kernel)
@@ -543,7 +548,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   };
 
   // per-thread accumulators (double across rows, float within a row)
-  double accS = 0.0, accZ = 0.0, accC = 0.0, accF = 0.0;
+  double accS = 0.0, accZ = 0.0, accC = 0.0, accF = 0.0, accMt = 0.0;
   float accM = -INFINITY;
   float argX = -INFINITY;   // hard-PSL argmax (value, key) of this thread
   int argK = 0x7fffffff;
@@ -711,8 +716,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       if (lrow) {
         const Mask inm = band & ~(k <= p.ml_k ? mlb : (Mask)0);
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
-        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f;
+        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f;
         const float gsc = scaleG * mult;
+        // match targets of rows +k and -k (K_MATCH; the host checked the window holds them)
+        const float* tgp = nullptr;
+        const float* tgn = nullptr;
+        if constexpr (KIND == K_MATCH) {
+          const float* tb0 = p.target + (size_t)b * p.target_stride;
+          tgp = tb0 + (size_t)(rowp < 0 ? 0 : rowp) * M;
+          tgn = tb0 + (size_t)(rown < 0 ? 0 : rown) * M;
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const bool in = (inm >> e) & 1;
@@ -739,6 +752,19 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             }
           } else if constexpr (KIND == K_ISL) {
             v[e] = cscale(v[e], in ? p.lam_isl * w * gsc : 0.f);   // G (x2 for a folded row pair)
+          } else if constexpr (KIND == K_MATCH) {
+            // f' of the folded pair (k, m), (-k, -m) / mult: lambda (2x - t1 - t2); a row that is
+            // its own mirror uses t2 = t1
+            const float x = p.normalize ? chi * invE2 : chi;
+            const int m = t + e * T;
+            const float t1 = tgp[(m + lay) & (M - 1)];
+            const float t2 = self ? t1 : tgn[(lay - m) & (M - 1)];
+            float fp = p.lam_isl * w + p.lam_match * (2.f * x - t1 - t2);
+            fp = in ? fp : 0.f;
+            rowF = fmaf(fp, chi, rowF);
+            v[e] = cscale(v[e], fp * gsc);
+            const float d1 = x - t1, d2 = self ? 0.f : x - t2;
+            rowMt += in ? d1 * d1 + d2 * d2 : 0.f;
           } else {
             const float x = p.normalize ? chi * invE2 : chi;
             float fp;
@@ -755,6 +781,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         if constexpr (KIND == K_ISL) rowF = p.lam_isl * rowS;
         accS += (double)(mult * rowS);
         accF += (double)(mult * rowF);
+        if constexpr (KIND == K_MATCH) accMt += (double)rowMt;
         if constexpr (FWD) {
           if (want_lse && rowM > -INFINITY) {
             if (rowM > accM) {
@@ -907,6 +934,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     }
     int K0 = 0x7fffffff;
     if constexpr (KIND == K_FWDA) K0 = block_argmax_key<THREADS>(argX, argK, scratch);
+    double Mt0 = 0.0;
+    if constexpr (KIND == K_MATCH) Mt0 = block_sum<THREADS>(accMt, scratch);
     if (threadIdx.x == 0) {
       rec[0] = S0;
       rec[1] = (double)M0;
@@ -914,6 +943,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       rec[3] = C0;
       rec[4] = F0;
       rec[5] = (double)K0;
+      rec[6] = Mt0;
     }
   } else {
     if (threadIdx.x == 0) {
@@ -923,6 +953,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       rec[3] = 0.0;
       rec[4] = 0.0;
       rec[5] = (double)0x7fffffff;
+      rec[6] = 0.0;
     }
   }
 
@@ -1051,6 +1082,7 @@ struct FinalizeParams {
   int P, N, B;
   int normalize, grad_norm_term;
   float lam_isl, lam_psl, invT, T;
+  float lam_match;
   double* loss;                  // may be NULL
   float2* grad;                  // may be NULL
 };
@@ -1064,12 +1096,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
     const double e = warp_energy(sg, N, threadIdx.x);
     if (threadIdx.x == 0) {
       sh[0] = e;
-      double S = 0, Z = 0, F = 0;
+      double S = 0, Z = 0, F = 0, Mt = 0;
       double m = -INFINITY;
       for (int q = 0; q < f.P; ++q) {
         const double* rec = f.part + ((size_t)b * f.P + q) * kPart;
         S += rec[0];
         F += rec[4];
+        Mt += rec[6];
         lse_merge(m, Z, rec[1], rec[2], f.T);
       }
       sh[1] = F;
@@ -1082,6 +1115,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
         }
         double L = f.lam_isl * (f.normalize ? Sg / (e * e) : Sg);
         if (f.lam_psl != 0.f) L += f.lam_psl * (mg + (double)f.T * log(Zg));
+        if (f.lam_match != 0.f) L += f.lam_match * Mt;
         f.loss[b] = L;
       }
     }

@@ -39,6 +39,8 @@ class LossSpec:
     temperature: float = 0.01
     normalize: int = 1
     lambda_hpsl: float = 0.0
+    lambda_match: float = 0.0
+    target: Optional[torch.Tensor] = None      # fp32 [rows, M] or [B, rows, M], surface-window layout
     w_k: Optional[torch.Tensor] = None   # device float32 [2N-1], symmetric
     w_d: Optional[torch.Tensor] = None   # device float32 [M], symmetric
 
@@ -50,7 +52,9 @@ class LossSpec:
         return L.LossDesc(int(self.k_max), int(self.d_max), int(self.ml_k), int(self.ml_d),
                           _ptr(self.w_k), _ptr(self.w_d), float(self.lambda_isl),
                           float(self.lambda_psl), float(self.temperature), int(self.normalize),
-                          float(self.lambda_hpsl))
+                          float(self.lambda_hpsl), float(self.lambda_match), _ptr(self.target),
+                          int(self.target.shape[-1] * self.target.shape[-2]) if (self.target is not None and
+                                                                                self.target.dim() == 3) else 0)
 
 
 def _ptr(t: Optional[torch.Tensor]):

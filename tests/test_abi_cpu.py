@@ -101,7 +101,7 @@ def test_host_combine_partials_is_exact_lse_merge():
     import math
     lib = L.lib()
     T = 0.5
-    ld = L.LossDesc(1, 1, 0, 0, None, None, 1.0, 1.0, T, 1, 0.0)
+    ld = L.LossDesc(1, 1, 0, 0, None, None, 1.0, 1.0, T, 1, 0.0, 0.0, None, 0)
     # two shards, one waveform: shard sums of exp((x-m)/T) over {0.1, 0.3} and {0.7}
     sh = (L.Partials * 2)(L.Partials(1.0, 0.3, math.exp((0.1 - 0.3) / T) + 1.0, 0.0, 7.0, 0.0),
                           L.Partials(2.0, 0.7, 1.0, 0.0, 5.0, 0.0))
