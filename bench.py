@@ -144,6 +144,9 @@ def cpu_baseline(w: dict, budget_s: float = 12.0) -> dict:
         if w["N"] * w["M"] > 4096 * 8192:          # c5: the direct sum takes minutes per waveform
             s_small = s
             O.loss_and_grad_chunked(s_small, M, spec)
+        elif w.get("match"):
+            tgt = np.random.default_rng(b).random((2 * N - 1, M)) / M
+            O.match_loss_and_grad(s, M, spec, tgt, -(N - 1), "centered")
         else:
             per = w.get("periodic", False)
             O.loss_and_grad(s, M, spec, periodic=per)
@@ -176,6 +179,10 @@ def run_reference(args, w) -> None:
         for j in range(per_step):
             s = config_waveforms(w["cid"], batch=1, start=(i * per_step + j) % w["B"])[0]
             per = w.get("periodic", False)
+            if w.get("match"):
+                tgt = np.random.default_rng(j).random((2 * w["N"] - 1, w["M"])) / w["M"]
+                O.match_loss_and_grad(s, w["M"], spec, tgt, -(w["N"] - 1), "centered")
+                continue
             O.loss_and_grad(s, w["M"], spec, periodic=per)
             if w["cfg"]["surface"]:
                 O.surface(s, w["M"], w["cfg"]["surface"], "centered", periodic=per,
@@ -214,7 +221,7 @@ def main():
     ap.add_argument("--impl", default="graf", choices=["graf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0)
-    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward", "lpi"],
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward", "lpi", "match"],
                     help="forward: full-surface mode (graf_af_forward writes the config's surface, no loss)")
     ap.add_argument("--periodic", action="store_true",
                     help="the paper's circular surface (Eq. 2 / Alg. 1, SURVEY 8(f) NEXT-1); needs M == N")
@@ -240,6 +247,18 @@ def main():
         w["io_bytes"] = w["B"] * w["N"] * 8
         w["launches"] = 1
         w["note"] = "full-surface mode: graf_af_forward writes the surface; no loss or gradient"
+    if args.mode == "match":
+        # match loss ||x - x_target||^2 over the config's region (NEXT-3): one fused
+        # pass streaming a per-waveform fp32 target of the full surface window
+        w["loss"] = dict(w["loss"], lambda_isl=0.0, lambda_psl=0.0, normalize=1)
+        w["match"] = True
+        w["ffts"] = 2
+        w["rows"] = min(w["loss"]["k_max"], w["N"] - 1) + 1
+        w["flops"] = w["B"] * w["rows"] * 2 * 5.0 * w["M"] * math.log2(w["M"])
+        # algorithmic bytes: s + g + the target cells of the region (both mirrored rows)
+        w["surf_bytes"] = w["B"] * (2 * w["rows"] - 1) * min(w["M"], 2 * w["loss"]["d_max"] + 1) * 4
+        w["launches"] = 2
+        w["note"] = "match loss over the region, per-waveform fp32 target of the surface window (HBM-streamed)"
     if args.impl == "reference":
         return run_reference(args, w)
 
@@ -263,6 +282,12 @@ def main():
     s = s_host.to(dev)
     spec = graf.LossSpec.from_dict(w["loss"])
     out = w["cfg"]["surface"]
+    if w.get("match"):
+        out = None
+        spec.lambda_match = 1.0
+        g_ = torch.Generator(device=dev)
+        g_.manual_seed(1234 + rank)
+        spec.target = torch.rand((B, 2 * N - 1, M), generator=g_, device=dev) * (1.0 / M)
     ws = graf.graf.Workspace()
     grad = torch.empty((B, N), dtype=torch.complex64, device=dev)
     loss_out = torch.empty((B,), dtype=torch.float64, device=dev)

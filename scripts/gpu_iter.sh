@@ -14,3 +14,9 @@ timeout 600 python bench.py --config 2 --periodic --steps 10 --warmup 3 --no-cpu
 python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c2per.json')); r=d['roofline']; print('c2per', d['ms_per_step'], r['bound'], r['frac'])"
 timeout 600 python bench.py --mode lpi --steps 10 --warmup 3 > gpurun_out/bench_${TAG}_lpi.json 2> gpurun_out/bench_${TAG}_lpi.err
 python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_lpi.json')); print('lpi it/s', d['value'], 'full2000 ms', d['config']['full_2000_iterations_ms'], 'loss', d['config']['final_loss_median'])"
+timeout 600 python bench.py --config 2 --mode match --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c2match.json 2> gpurun_out/bench_${TAG}_c2match.err
+timeout 900 python bench.py --config 3 --mode match --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c3match.json 2> gpurun_out/bench_${TAG}_c3match.err
+python -c "
+import json
+for c in ('c2match','c3match'):
+    d=json.load(open('gpurun_out/bench_${TAG}_'+c+'.json')); r=d['roofline']; print(c, d['ms_per_step'], r['bound'], r['frac'])"
