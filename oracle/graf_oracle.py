@@ -53,7 +53,8 @@ __all__ = [
     "lag_products", "ambiguity", "region", "loss_terms", "loss",
     "loss_and_grad", "adjoint", "correlate", "surface", "loss_and_grad_chunked",
     "periodic_ambiguity", "hard_psl_and_grad", "spectral_variance_and_grad", "phase_grad",
-    "adam_step", "lpi_loss_and_grad", "match_loss_and_grad",
+    "adam_step", "lpi_loss_and_grad", "match_loss_and_grad", "cross_lag_products", "cross_ambiguity",
+    "cross_correlate", "cross_adjoint", "cross_loss_and_grad",
 ]
 
 
@@ -472,3 +473,80 @@ def match_loss_and_grad(s: np.ndarray, M: int, spec: LossSpec, target: np.ndarra
     if spec.normalize:
         g = g - (2.0 / E ** 3) * float(np.sum(fp * chi)) * s
     return L, g
+
+
+# ---------------------------------------------------------------------------
+# Cross-ambiguity (P:L546 MIMO):
+#   X[k,m] = sum_n s1[n] conj(s2[n-k]) exp(-2j pi m n / M)   (aperiodic, k in +-(N-1))
+# normalised by E1*E2 (reading R25: |X| <= sqrt(E1 E2), equal to E^2 when s1 = s2).
+# Losses over Omega_s as for the auto surface; no row folding (no symmetry).
+# ---------------------------------------------------------------------------
+def cross_lag_products(s1: np.ndarray, s2: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """R[i, n] = s1[n] conj(s2[n-k_i]) for 0 <= n-k_i < N, else 0."""
+    s1 = np.asarray(s1, dtype=np.complex128)
+    s2 = np.asarray(s2, dtype=np.complex128)
+    n = s1.shape[0]
+    R = np.zeros((len(rows), n), dtype=np.complex128)
+    for i, k in enumerate(rows):
+        k = int(k)
+        lo, hi = max(0, k), min(n, n + k)
+        if lo < hi:
+            R[i, lo:hi] = s1[lo:hi] * np.conj(s2[lo - k:hi - k])
+    return R
+
+
+def cross_ambiguity(s1, s2, M: int, rows=None, bins=None) -> np.ndarray:
+    n = len(s1)
+    rows = delay_rows(n) if rows is None else np.asarray(rows)
+    bins = np.arange(M) if bins is None else np.asarray(bins)
+    return cross_lag_products(s1, s2, rows) @ dft_matrix(n, M, bins)
+
+
+def cross_correlate(s1, s2, H: np.ndarray, rows: np.ndarray):
+    """(g1, g2): g1[p] = sum_k H[k,p] s2[p-k] (dX*-side w.r.t. s1*), g2[p] = sum_k conj(H[k,p+k]) s1[p+k]."""
+    s1 = np.asarray(s1, dtype=np.complex128)
+    s2 = np.asarray(s2, dtype=np.complex128)
+    n = s1.shape[0]
+    g1 = np.zeros(n, dtype=np.complex128)
+    g2 = np.zeros(n, dtype=np.complex128)
+    for i, k in enumerate(rows):
+        k = int(k)
+        lo, hi = max(0, k), min(n, n + k)
+        if lo >= hi:
+            continue
+        g1[lo:hi] += H[i, lo:hi] * s2[lo - k:hi - k]
+        g2[lo - k:hi - k] += np.conj(H[i, lo:hi]) * s1[lo:hi]
+    return g1, g2
+
+
+def cross_adjoint(s1, s2, M: int, G: np.ndarray, rows: np.ndarray, bins=None):
+    n = len(s1)
+    bins = np.arange(M) if bins is None else np.asarray(bins)
+    H = np.asarray(G, dtype=np.complex128) @ dft_matrix(n, M, bins, sign=+1).T
+    return cross_correlate(s1, s2, H, rows)
+
+
+def cross_loss_and_grad(s1, s2, M: int, spec: LossSpec):
+    """(L, g1 = dL/ds1*, g2 = dL/ds2*) for L = lambda_isl ISL + lambda_psl softPSL on X."""
+    s1 = np.asarray(s1, dtype=np.complex128)
+    s2 = np.asarray(s2, dtype=np.complex128)
+    n = s1.shape[0]
+    rows, bins, mask, w = region(n, M, spec)
+    E1, E2 = energy(s1), energy(s2)
+    A = cross_ambiguity(s1, s2, M, rows, bins)
+    chi = A.real ** 2 + A.imag ** 2
+    x = chi / (E1 * E2) if spec.normalize else chi
+    S = float(np.sum(w[mask] * chi[mask]))
+    T = spec.temperature
+    c = float(np.max(x[mask]))
+    lse = c + T * np.log(float(np.sum(np.exp((x[mask] - c) / T))))
+    L = spec.lambda_isl * (S / (E1 * E2) if spec.normalize else S) + spec.lambda_psl * lse
+    fp = np.zeros_like(chi)
+    fp[mask] = spec.lambda_isl * w[mask] + spec.lambda_psl * np.exp((x[mask] - lse) / T)
+    G = fp * A / (E1 * E2) if spec.normalize else fp * A
+    g1, g2 = cross_adjoint(s1, s2, M, G, rows, bins)
+    if spec.normalize:
+        F = float(np.sum(fp * chi))
+        g1 = g1 - F / (E1 ** 2 * E2) * s1
+        g2 = g2 - F / (E1 * E2 ** 2) * s2
+    return L, g1, g2

@@ -538,3 +538,50 @@ def test_match_loss_pins(periodic, layout):
     fd = _fd(lambda z: O.match_loss_and_grad(z, M, spec, tgt, kb, layout, periodic)[0], s)
     np.testing.assert_allclose(2 * g, fd, atol=1e-6 * max(1.0, np.abs(fd).max()))
     assert abs(np.vdot(g, s).imag) < 1e-10 * max(1, np.abs(g).max())
+
+
+# ---------------------------------------------------------------- cross-ambiguity (NEXT-4)
+def test_cross_reduces_to_auto_and_swap_identity():
+    n, M = 9, 16
+    s = rs(n, 130)
+    rows = np.arange(-(n - 1), n)
+    np.testing.assert_allclose(O.cross_ambiguity(s, s, M), O.ambiguity(s, M), atol=1e-13)
+    spec = O.LossSpec(k_max=5, d_max=6, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=0.5, temperature=0.05,
+                      normalize=1)
+    L, g1, g2 = O.cross_loss_and_grad(s, s, M, spec)
+    La, ga, _ = O.loss_and_grad(s, M, spec)
+    assert abs(L - La) < 1e-13 * abs(La)
+    np.testing.assert_allclose(g1 + g2, ga, atol=1e-12 * np.abs(ga).max())
+    # X_21[-k, m] = W^{-mk} conj(X_12[k, -m]);  Cauchy-Schwarz |X| <= sqrt(E1 E2)
+    s2 = rs(n, 131)
+    X12 = O.cross_ambiguity(s, s2, M)
+    X21 = O.cross_ambiguity(s2, s, M)
+    m = np.arange(M)
+    for i, k in enumerate(rows):
+        ph = np.exp(2j * np.pi * ((m * k) % M) / M)
+        np.testing.assert_allclose(X21[row(rows, -k)], ph * np.conj(X12[i, (-m) % M]), atol=1e-12)
+    assert np.abs(X12).max() <= np.sqrt(O.energy(s) * O.energy(s2)) * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("normalize", [1, 0])
+def test_cross_gradients_central_differences(normalize):
+    n, M = 7, 8
+    s1, s2 = rs(n, 132), rs(n, 133)
+    spec = O.LossSpec(k_max=4, d_max=3, ml_k=0, ml_d=0, lambda_isl=1.0, lambda_psl=0.7, temperature=0.05 if
+                      normalize else 2.0, normalize=normalize)
+    L, g1, g2 = O.cross_loss_and_grad(s1, s2, M, spec)
+    fd1 = _fd(lambda z: O.cross_loss_and_grad(z, s2, M, spec)[0], s1)
+    fd2 = _fd(lambda z: O.cross_loss_and_grad(s1, z, M, spec)[0], s2)
+    np.testing.assert_allclose(2 * g1, fd1, atol=1e-6 * max(1.0, np.abs(fd1).max()))
+    np.testing.assert_allclose(2 * g2, fd2, atol=1e-6 * max(1.0, np.abs(fd2).max()))
+
+
+def test_cross_adjoint_inner_product_identity():
+    n, M = 10, 16
+    s1, s2, d1, d2 = rs(n, 134), rs(n, 135), rs(n, 136), rs(n, 137)
+    rows = np.arange(-(n - 1), n)
+    G = rs(len(rows) * M, 138).reshape(len(rows), M)
+    # X is bilinear in (s1, conj s2): the exact linearisation in (d1, d2)
+    lin = (O.cross_ambiguity(s1 + d1, s2 + d2, M) - O.cross_ambiguity(s1 - d1, s2 - d2, M)) / 2
+    g1, g2 = O.cross_adjoint(s1, s2, M, G, rows)
+    assert abs(np.vdot(G, lin).real - (np.vdot(g1, d1).real + np.vdot(g2, d2).real)) < 1e-10
