@@ -163,6 +163,26 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
 graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA,
                              void* grad, void* ws, size_t ws_bytes, void* stream);
 
+/* Cross-ambiguity ("cross-ambiguity" for MIMO):
+ *   X[k,m] = sum_n s1[n] conj(s2[n-k]) exp(-2 pi j m n / M),  k in [-(N-1), N-1],
+ * the same kernels with the second waveform staged beside the first.  Rows are NOT
+ * folded (X has no mirror symmetry).  Normalised quantities use E1 E2 in place of
+ * E^2 (reading R25: |X| <= sqrt(E1 E2), = E^2 when s1 = s2); the surface with
+ * normalize_output holds X / sqrt(E1 E2).  The loss call returns both Wirtinger
+ * gradients: grad1 = dL/ds1*, grad2 = dL/ds2* (complex64 [B][N]).  v1 limits
+ * (GRAF_EUNSUPPORTED otherwise): aperiodic, unsharded, M <= 4096, unweighted ISL
+ * and soft-PSL (no hard PSL / match).  Workspace: graf_xaf_workspace_bytes. */
+size_t graf_xaf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss);
+graf_status graf_xaf_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s1,
+                             const void* s2, void* surface, graf_partials* partials, void* ws,
+                             size_t ws_bytes, void* stream);
+graf_status graf_xaf_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s1,
+                               const void* s2, const graf_partials* global, double* loss_out,
+                               void* grad1, void* grad2, void* surface, void* ws, size_t ws_bytes,
+                               void* stream);
+graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void* s2, const void* dA,
+                              void* grad1, void* grad2, void* ws, size_t ws_bytes, void* stream);
+
 /* Spectral variance of each waveform (the paper's section-7 LPI term, L417):
  *   SV_b = var{ |F s_b|^2 / sum |F s_b|^2 } over the N DFT bins, unbiased (N - 1;
  *   the paper's PyTorch var, reading R22), F the length-N DFT,

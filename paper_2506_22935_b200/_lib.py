@@ -18,7 +18,8 @@ DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
 EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_workspace_bytes",
            "graf_af_forward", "graf_af_loss_grad", "graf_af_backward", "graf_combine_partials",
            "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
-           "graf_phase_adam_step")
+           "graf_phase_adam_step", "graf_xaf_workspace_bytes", "graf_xaf_forward", "graf_xaf_loss_grad",
+           "graf_xaf_backward")
 
 
 class AfDesc(ctypes.Structure):
@@ -76,6 +77,17 @@ def lib() -> ctypes.CDLL:
         L.graf_combine_partials.restype = c_int32
         L.graf_combine_partials.argtypes = [POINTER(LossDesc), c_void_p, c_int32, c_int64, c_void_p, c_int32,
                                             c_void_p]
+        L.graf_xaf_workspace_bytes.restype = c_size_t
+        L.graf_xaf_workspace_bytes.argtypes = [POINTER(AfDesc), POINTER(LossDesc)]
+        L.graf_xaf_forward.restype = c_int32
+        L.graf_xaf_forward.argtypes = [POINTER(AfDesc), POINTER(LossDesc), c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_size_t, c_void_p]
+        L.graf_xaf_loss_grad.restype = c_int32
+        L.graf_xaf_loss_grad.argtypes = [POINTER(AfDesc), POINTER(LossDesc), c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+        L.graf_xaf_backward.restype = c_int32
+        L.graf_xaf_backward.argtypes = [POINTER(AfDesc), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_size_t, c_void_p]
         L.graf_spectral_variance.restype = c_int32
         L.graf_spectral_variance.argtypes = [c_int64, c_int32, c_void_p, c_float, c_void_p, c_void_p, c_void_p,
                                              c_int32, c_void_p]

@@ -2,6 +2,8 @@
 // workspace layout and the kernel sequences of each entry point.
 #include <cuda_runtime.h>
 
+#define GRAF_API_UNIT 1   // this unit defines the non-template kernels of graf_kernels.cuh
+
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -11,13 +13,30 @@
 #include <vector>
 
 #include "../../include/graf.h"
-#include "graf_kernels.cuh"
+#include "graf_launch.cuh"
 
 namespace graf {
+thread_local int t_launches = 0;   // kernels / memsets enqueued by this thread's last entry-point call
+std::vector<TwUpload>& tw_uploaders() {
+  static std::vector<TwUpload> v;   // filled by the row-kernel translation units at load time
+  return v;
+}
 namespace {
 
 thread_local std::string t_last_error;
-thread_local int t_launches = 0;   // kernels / memsets enqueued by this thread's last entry-point call
+// cross-ambiguity context of the current graf_xaf_* call (NULL for the auto entry points)
+thread_local const void* t_s2 = nullptr;
+thread_local void* t_grad2 = nullptr;
+struct CrossScope {
+  CrossScope(const void* s2, void* g2) {
+    t_s2 = s2;
+    t_grad2 = g2;
+  }
+  ~CrossScope() {
+    t_s2 = nullptr;
+    t_grad2 = nullptr;
+  }
+};
 thread_local cudaEvent_t t_prof_start = nullptr, t_prof_stop = nullptr;
 
 cudaError_t prof_mark(bool start, cudaStream_t st) {
@@ -48,7 +67,6 @@ graf_status cuda_fail(cudaError_t e, const char* what) {
 // ---------------------------------------------------------------------------
 // one-time per-device twiddle table (immutable afterwards)
 // ---------------------------------------------------------------------------
-constexpr int kMaxDev = 64;
 std::once_flag g_tw_once[kMaxDev];
 cudaError_t g_tw_err[kMaxDev];
 
@@ -64,34 +82,14 @@ cudaError_t ensure_twiddles() {
       const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)i / kMaxM;
       h[i] = make_float2((float)cosl(a), (float)sinl(a));
     }
-    g_tw_err[dev] = cudaMemcpyToSymbol(g_tw, h.data(), sizeof(float2) * kMaxM);
+    // every translation unit holds its own copy of the table (graf_fft.cuh)
+    cudaError_t e0 = cudaMemcpyToSymbol(g_tw, h.data(), sizeof(float2) * kMaxM);
+    for (auto up : tw_uploaders())
+      if (e0 == cudaSuccess) e0 = up(h.data());
+    g_tw_err[dev] = e0;
   });
   return g_tw_err[dev];
 }
-
-// ---------------------------------------------------------------------------
-// launch plan
-// ---------------------------------------------------------------------------
-struct Plan {
-  int M = 0, threads = 0, S = 0, T = 0, P = 1, Pbound = 1;
-  int U = 0, row_lo = 0, row_step = 1;
-  bool fixedP = false;
-  bool s_smem = true, g_smem = true;
-  size_t smem = 0;
-  // surface staging for bulk async row stores: per-slot floats,
-  // whether the rows qualify, and whether they fit the slot's exchange buffer (alias)
-  int stg_floats = 0;
-  bool bulk_ok = false, alias_ok = false;
-  size_t smem_stg = 0;
-  int bulk_mode = -1;   // decided at the first launch of a call: 0 direct, 1 dedicated, 2 alias
-  // left-padded gradient accumulators (M == N loss calls), if they cost no resident CTA
-  bool gpad_ok = false;
-  size_t smem_gpad = 0;
-  int gpad_mode = -1;
-  // fused finalize (K_ISL only): requested by the caller, granted when P <= 8
-  bool fuse_req = false, fused = false;
-  size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
-};
 
 struct CfgInfo {
   int M, E, T, S, threads, XS, tab1;
@@ -125,7 +123,6 @@ bool cfg_for(int M, CfgInfo* ci) {
   }
 }
 
-constexpr int kNumSM = 148;  // B200; the plan is a pure function of the descriptors
 
 bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -210,6 +207,8 @@ enum class Kind { Forward, LossGrad, Backward };
 
 Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   Plan pl;
+  const bool cross = (t_s2 != nullptr);
+  pl.cross = cross;
   CfgInfo ci;
   cfg_for(af->m, &ci);
   pl.M = af->m;
@@ -229,7 +228,17 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
     const bool surf = af->out_kind != GRAF_OUT_NONE;
     const int kfold = af->periodic ? N / 2 : N - 1;   // largest folded delay
     const int kloss = L ? std::min(L->k_max, kfold) : -1;
-    if (surf) {
+    if (cross) {
+      // unfolded rows: the loss rows [-kloss, kloss] and the surface window
+      int lo = L ? -kloss : INT32_MAX, hi = L ? kloss : INT32_MIN;
+      if (surf) {
+        lo = std::min(lo, af->k_begin);
+        hi = std::max(hi, af->k_end - 1);
+      }
+      pl.row_lo = lo;
+      pl.row_step = 1;
+      pl.U = (L || surf) ? hi - lo + 1 : 0;
+    } else if (surf) {
       int lo, hi;
       if (af->periodic) {   // every folded residue pair may meet the window
         lo = 0;
@@ -252,9 +261,11 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
       pl.U = 0;
     }
   }
-  pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
-                              (grad && ci.g_smem ? (size_t)ci.S * N : 0) + (size_t)ci.tab1);
-  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512 && !af->periodic) {
+  const size_t nsig = cross ? 2 : 1;   // staged waveforms and gradient accumulator sets
+  pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) +
+                              (cross ? (size_t)((N + std::max(af->m, 2 * N) + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
+                              (grad && ci.g_smem ? nsig * ci.S * N : 0) + (size_t)ci.tab1);
+  if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512 && !af->periodic && !cross) {
     pl.gpad_ok = true;
     pl.smem_gpad = sizeof(float2) * (size_t)ci.S * N;
   }
@@ -283,7 +294,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   pl.off_part = off;
   off = align256(off + sizeof(double) * kPart * (size_t)B * pl.Pbound);
   pl.off_gpart = off;
-  if (grad) off = align256(off + sizeof(float2) * (size_t)B * pl.Pbound * N);
+  if (grad) off = align256(off + (cross ? 2 : 1) * sizeof(float2) * (size_t)B * pl.Pbound * N);
   pl.off_comb = off;
   off = align256(off + sizeof(graf_partials) * (size_t)B);
   pl.off_spad = off;
@@ -292,165 +303,27 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   return pl;
 }
 
-// Cost model: waves x (row iterations + CTA setup), setup ~ one row iteration.
-int choose_P(const Plan& pl, long long B, int occ, int nsm) {
-  const long long cap = (long long)nsm * std::max(occ, 1);
-  int best = 1;
-  double best_t = 1e300;
-  for (int P = 1; P <= pl.Pbound; ++P) {
-    const long long ctas = (long long)P * B;
-    const double waves = (double)((ctas + cap - 1) / cap);
-    const double iters = (double)((pl.U + (long long)P * pl.S - 1) / ((long long)P * pl.S));
-    const double t = waves * (iters + 1.0);
-    if (t < best_t - 1e-9) {
-      best_t = t;
-      best = P;
-    }
-  }
-  return best;
-}
-
-template <int M, int KIND, bool WGT>
-cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
-  static std::once_flag once[kMaxDev];
-  static cudaError_t attr_err[kMaxDev];
-  static int sm_count[kMaxDev];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  std::call_once(once[dev], [dev] {
-    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M, KIND, WGT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (attr_err[dev] == cudaSuccess)
-      attr_err[dev] = cudaDeviceGetAttribute(&sm_count[dev], cudaDevAttrMultiProcessorCount, dev);
-  });
-  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
-  *nsm = sm_count[dev];
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT>, Cfg<M>::THREADS, smem);
-}
-
-template <int M, int KIND, bool WGT>
-cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
-  int occ = 1, nsm = kNumSM;
-  // (also sets the instantiation's large-shared-memory attribute, once per device)
-  cudaError_t e0 = kernel_occupancy<M, KIND, WGT>(pl.smem, &occ, &nsm);
-  if (e0 != cudaSuccess) return e0;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  size_t smem = pl.smem;
-  rp.gpad = 0;
-  if (pl.gpad_ok && KIND != K_ADJ && KIND != K_FWD && KIND != K_FWDA) {
-    if (pl.gpad_mode < 0) {
-      int occ_g = 0;
-      const bool fits = pl.smem + pl.smem_gpad <= 227 * 1024;
-      if (fits) {
-        e0 = kernel_occupancy<M, KIND, WGT>(pl.smem + pl.smem_gpad, &occ_g, &nsm);
-        if (e0 != cudaSuccess) return e0;
-      }
-      pl.gpad_mode = (fits && occ_g >= occ) ? 1 : 0;
-    }
-    if (pl.gpad_mode == 1) {
-      rp.gpad = 1;
-      smem += pl.smem_gpad;
-    }
-  }
-  if (rp.surface && pl.bulk_ok) {
-    if (pl.bulk_mode < 0) {
-      // dedicated staging unless it costs resident CTAs and the exchange buffer can hold the rows
-      int occ_d = 0;
-      const bool fits = smem + pl.smem_stg <= 227 * 1024;
-      if (fits) {
-        e0 = kernel_occupancy<M, KIND, WGT>(smem + pl.smem_stg, &occ_d, &nsm);
-        if (e0 != cudaSuccess) return e0;
-      }
-      pl.bulk_mode = (fits && (occ_d >= occ || !pl.alias_ok) && occ_d >= 1) ? 1 : pl.alias_ok ? 2 : 0;
-    }
-    rp.bulk = pl.bulk_mode;
-    rp.stg_floats = pl.stg_floats;
-    if (rp.bulk == 1) {
-      smem += pl.smem_stg;
-      e0 = kernel_occupancy<M, KIND, WGT>(smem, &occ, &nsm);
-      if (e0 != cudaSuccess) return e0;
-    }
-  } else {
-    rp.bulk = 0;
-  }
-  if (!pl.fixedP) {
-    pl.P = choose_P(pl, B, occ, nsm);
-    pl.fixedP = true;   // later passes of the same call reuse it
-  }
-  rp.fuse = 0;
-  if (KIND == K_ISL && pl.fuse_req && pl.P >= 2 && pl.P <= 8) {   // (P = 1: measured slower as a cluster launch)
-    rp.fuse = 1;
-    pl.fused = true;
-  }
-  for (int b0 = 0; b0 < B; b0 += 65535) {
-    rp.b0 = b0;
-    dim3 grid(pl.P, std::min(65535, B - b0));
-    rp.smem_bytes = (int)smem;
-    if (rp.fuse) {
-      // the P CTAs of a waveform form one thread-block cluster (rank 0 finalizes)
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = grid;
-      cfg.blockDim = dim3(pl.threads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = (unsigned)pl.P;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, af_rows_kernel<M, KIND, WGT>, rp);
-      if (e != cudaSuccess) return e;
-    } else {
-      af_rows_kernel<M, KIND, WGT><<<grid, pl.threads, smem, st>>>(rp);
-    }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    ++t_launches;
-  }
-  return cudaSuccess;
-}
-
-template <int M>
-cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind, bool wgt) {
-  switch (kind) {
-    case K_FWD:
-      if (rp.want_argmax)
-        return wgt ? launch_kernel<M, K_FWDA, true>(pl, rp, B, st) : launch_kernel<M, K_FWDA, false>(pl, rp, B, st);
-      return wgt ? launch_kernel<M, K_FWD, true>(pl, rp, B, st) : launch_kernel<M, K_FWD, false>(pl, rp, B, st);
-    case K_ISL: return wgt ? launch_kernel<M, K_ISL, true>(pl, rp, B, st) : launch_kernel<M, K_ISL, false>(pl, rp, B, st);
-    case K_PASS2:
-      return wgt ? launch_kernel<M, K_PASS2, true>(pl, rp, B, st) : launch_kernel<M, K_PASS2, false>(pl, rp, B, st);
-    case K_ADJ: return launch_kernel<M, K_ADJ, false>(pl, rp, B, st);
-    case K_MATCH:
-      return wgt ? launch_kernel<M, K_MATCH, true>(pl, rp, B, st) : launch_kernel<M, K_MATCH, false>(pl, rp, B, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
 
 cudaError_t launch_rows(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind) {
-  const bool wgt = (rp.w_k != nullptr) || (rp.w_d != nullptr);
-#ifdef GRAF_ONLY_M  // tuning builds (scripts/tune.py) instantiate a single size
-  if (pl.M == GRAF_ONLY_M) return launch_rows_t<GRAF_ONLY_M>(pl, rp, B, st, kind, wgt);
+#ifdef GRAF_ONLY_M  // tuning builds (scripts/tune.py) link a single size
+  if (pl.M == GRAF_ONLY_M) return launch_rows_size<GRAF_ONLY_M>(pl, rp, B, st, kind);
   return cudaErrorNotSupported;
 #else
   switch (pl.M) {
-    case 2: return launch_rows_t<2>(pl, rp, B, st, kind, wgt);
-    case 4: return launch_rows_t<4>(pl, rp, B, st, kind, wgt);
-    case 8: return launch_rows_t<8>(pl, rp, B, st, kind, wgt);
-    case 16: return launch_rows_t<16>(pl, rp, B, st, kind, wgt);
-    case 32: return launch_rows_t<32>(pl, rp, B, st, kind, wgt);
-    case 64: return launch_rows_t<64>(pl, rp, B, st, kind, wgt);
-    case 128: return launch_rows_t<128>(pl, rp, B, st, kind, wgt);
-    case 256: return launch_rows_t<256>(pl, rp, B, st, kind, wgt);
-    case 512: return launch_rows_t<512>(pl, rp, B, st, kind, wgt);
-    case 1024: return launch_rows_t<1024>(pl, rp, B, st, kind, wgt);
-    case 2048: return launch_rows_t<2048>(pl, rp, B, st, kind, wgt);
-    case 4096: return launch_rows_t<4096>(pl, rp, B, st, kind, wgt);
-    case 8192: return launch_rows_t<8192>(pl, rp, B, st, kind, wgt);
-    case 16384: return launch_rows_t<16384>(pl, rp, B, st, kind, wgt);
+    case 2: return launch_rows_size<2>(pl, rp, B, st, kind);
+    case 4: return launch_rows_size<4>(pl, rp, B, st, kind);
+    case 8: return launch_rows_size<8>(pl, rp, B, st, kind);
+    case 16: return launch_rows_size<16>(pl, rp, B, st, kind);
+    case 32: return launch_rows_size<32>(pl, rp, B, st, kind);
+    case 64: return launch_rows_size<64>(pl, rp, B, st, kind);
+    case 128: return launch_rows_size<128>(pl, rp, B, st, kind);
+    case 256: return launch_rows_size<256>(pl, rp, B, st, kind);
+    case 512: return launch_rows_size<512>(pl, rp, B, st, kind);
+    case 1024: return launch_rows_size<1024>(pl, rp, B, st, kind);
+    case 2048: return launch_rows_size<2048>(pl, rp, B, st, kind);
+    case 4096: return launch_rows_size<4096>(pl, rp, B, st, kind);
+    case 8192: return launch_rows_size<8192>(pl, rp, B, st, kind);
+    case 16384: return launch_rows_size<16384>(pl, rp, B, st, kind);
     default: return cudaErrorInvalidValue;
   }
 #endif
@@ -504,6 +377,10 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
   char* w = static_cast<char*>(ws);
   rp.part = reinterpret_cast<double*>(w + pl.off_part);
   rp.gpart = reinterpret_cast<float2*>(w + pl.off_gpart);
+  if (pl.cross) {
+    rp.s2 = static_cast<const float2*>(t_s2);
+    rp.gpart2 = rp.gpart + (size_t)af->batch * pl.Pbound * af->n;
+  }
   rp.s_pad = pl.s_smem ? nullptr : reinterpret_cast<const float2*>(w + pl.off_spad);
   return rp;
 }
@@ -571,6 +448,11 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
   f.lam_match = L ? L->lambda_match : 0.f;
   f.loss = loss;
   f.grad = static_cast<float2*>(grad);
+  if (pl.cross) {
+    f.s2 = static_cast<const float2*>(t_s2);
+    f.gpart2 = f.gpart + (size_t)af->batch * pl.Pbound * af->n;
+    f.grad2 = static_cast<float2*>(t_grad2);
+  }
   const long long B = af->batch;
   for (long long b0 = 0; b0 < B; b0 += 65535) {
     FinalizeParams fc = f;
@@ -581,6 +463,11 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
     fc.global = global ? global + b0 : nullptr;
     fc.loss = loss ? loss + b0 : nullptr;
     fc.grad = grad ? f.grad + b0 * af->n : nullptr;
+    if (f.s2) {
+      fc.s2 = f.s2 + b0 * af->n;
+      fc.gpart2 = f.gpart2 + b0 * pl.P * (long long)af->n;
+      fc.grad2 = f.grad2 ? f.grad2 + b0 * af->n : nullptr;
+    }
     fc.B = (int)nb;
     finalize_kernel<<<(unsigned)nb, 256, 0, st>>>(fc);
     cudaError_t e = cudaGetLastError();
@@ -603,6 +490,16 @@ graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L,
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++t_launches;
   return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "partials_reduce_kernel launch");
+}
+
+graf_status check_cross(const graf_af_desc* af, const graf_loss_desc* L, const void* s2) {
+  if (!s2 || !aligned8(s2)) return fail(GRAF_EINVAL, "s2 is NULL or not 8-byte aligned");
+  if (af->periodic) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity is aperiodic in v1");
+  if (af->shard_count > 1) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity is unsharded in v1");
+  if (af->m > 4096) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity needs M <= 4096 in v1");
+  if (L && (L->lambda_hpsl != 0.f || L->lambda_match != 0.f || L->w_k || L->w_d))
+    return fail(GRAF_EUNSUPPORTED, "cross-ambiguity losses: unweighted ISL and soft-PSL in v1");
+  return GRAF_OK;
 }
 
 // hard PSL term (loss and argmax subgradient) from the combined partials
@@ -806,6 +703,44 @@ graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* 
   if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (adjoint) launch");
   prof_mark(false, cs);
   return run_finalize(af, nullptr, pl, s, ws, nullptr, nullptr, grad, false, cs);
+}
+
+size_t graf_xaf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) {
+  CrossScope cross(reinterpret_cast<const void*>(16), nullptr);   // any non-NULL: plan as cross
+  return graf_workspace_bytes(af, loss);
+}
+
+graf_status graf_xaf_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s1, const void* s2,
+                             void* surface, graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
+  t_launches = 0;
+  if (!af) return fail(GRAF_EINVAL, "af descriptor is NULL");
+  graf_status st = check_cross(af, loss, s2);
+  if (st) return st;
+  CrossScope cross(s2, nullptr);
+  return graf_af_forward(af, loss, s1, surface, partials, ws, ws_bytes, stream);
+}
+
+graf_status graf_xaf_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s1, const void* s2,
+                               const graf_partials* global, double* loss_out, void* grad1, void* grad2,
+                               void* surface, void* ws, size_t ws_bytes, void* stream) {
+  t_launches = 0;
+  if (!af) return fail(GRAF_EINVAL, "af descriptor is NULL");
+  graf_status st = check_cross(af, loss, s2);
+  if (st) return st;
+  if (!grad2 || !aligned8(grad2)) return fail(GRAF_EINVAL, "grad2 is NULL or not 8-byte aligned");
+  CrossScope cross(s2, grad2);
+  return graf_af_loss_grad(af, loss, s1, global, loss_out, grad1, surface, ws, ws_bytes, stream);
+}
+
+graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void* s2, const void* dA, void* grad1,
+                              void* grad2, void* ws, size_t ws_bytes, void* stream) {
+  t_launches = 0;
+  if (!af) return fail(GRAF_EINVAL, "af descriptor is NULL");
+  graf_status st = check_cross(af, nullptr, s2);
+  if (st) return st;
+  if (!grad2 || !aligned8(grad2)) return fail(GRAF_EINVAL, "grad2 is NULL or not 8-byte aligned");
+  CrossScope cross(s2, grad2);
+  return graf_af_backward(af, s1, dA, grad1, ws, ws_bytes, stream);
 }
 
 graf_status graf_set_profile_events(void* start, void* stop) {

@@ -31,9 +31,10 @@ namespace graf {
 constexpr int kMaxM = 16384;
 
 // M-th roots of unity table, g_tw[i] = exp(-2 pi i * i / kMaxM), float32
-// correctly rounded from extended precision on the host (graf_api.cu).  The
-// library is one translation unit, so the definition lives here.
-__device__ float2 g_tw[kMaxM];
+// correctly rounded from extended precision on the host (graf_api.cu).  Each
+// translation unit of the library (graf_api.cu, graf_rows_*.cu) holds its own
+// copy; ensure_twiddles() uploads all of them.
+static __device__ float2 g_tw[kMaxM];
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }

@@ -68,6 +68,9 @@ struct RowParams {
   // (delay index from key_lo) * M + raw Doppler bin, ties -> lowest key (reading R23)
   int want_argmax;
   int key_lo;
+  // cross-ambiguity (CROSS kernels): X = sum s[n] conj(s2[n-k]) W^{mn}; rows unfolded
+  const float2* s2;    // [B][N]
+  float2* gpart2;      // [B][P][N] partial dL/ds2*
   // match loss (K_MATCH): target laid out like the surface window, per waveform stride
   float lam_match;
   const float* target;
@@ -434,7 +437,11 @@ __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi
   return hi & ~lo;
 }
 
-template <int M, int KIND, bool WGT>
+// CROSS: cross-ambiguity of two waveforms: rows unfolded (no
+// mirror symmetry), lag product s[n] conj(s2[n-k]), normalisation by E1 E2 (reading
+// R25), and the correlation split into dL/ds* (term 1, with s2) and dL/ds2* (term 2,
+// with s) accumulated separately.
+template <int M, int KIND, bool WGT, bool CROSS = false>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
@@ -459,9 +466,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   double* red = reinterpret_cast<double*>(smem);
   float2* s_pad = smem + 64;
   const int NP2 = (N + M + 1) & ~1;
-  float2* xch = s_pad + (C::S_SMEM ? NP2 : 0);
+  // CROSS: the second waveform, zero-padded over [-N, max(M, 2N)): unfolded rows k < 0 read
+  // s2[n - k] up to n - k = 2N - 2 where s[n] != 0
+  float2* s2_pad = s_pad + (C::S_SMEM ? NP2 : 0);
+  const int NP2X = (N + (M > 2 * N ? M : 2 * N) + 1) & ~1;
+  float2* xch = s2_pad + (CROSS ? NP2X : 0);
   float2* gacc_sh = xch + S * XS;
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
+  const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
   // per-slot accumulator stride: N, or 2N with N zero-padding on the left (p.gpad: folded
   // rows with M == N need no support predicates, out-of-support terms land in the pad)
   // (compiled for the small sizes only: at M >= 1024 the padded accumulators never fit
@@ -469,9 +481,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   constexpr bool kGpadSizes = (M <= 512);
   const int GS = p.gpad ? 2 * N : N;
   float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * GS + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
+  constexpr int NG = CROSS ? 2 : 1;                           // accumulator sets (CROSS: g1, g2)
+  float2* gacc2 = gacc + (size_t)S * GS;                      // CROSS: dL/ds2* accumulators
   // surface staging (bulk path): after the gradient accumulators, 16-byte aligned
   float* stg = reinterpret_cast<float*>(
-                   xch + (((size_t)S * XS + (GRAD && C::G_SMEM ? (size_t)S * GS : 0) + 1) & ~(size_t)1)) +
+                   xch + (((size_t)S * XS + (GRAD && C::G_SMEM ? (size_t)NG * S * GS : 0) + 1) & ~(size_t)1)) +
                (size_t)slot * p.stg_floats;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
@@ -479,10 +493,15 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     for (int i = threadIdx.x; i < N + M; i += THREADS)
       // aperiodic: N zeros on the left; periodic: a copy of s, so s_pad[n - k] = s[(n - k) mod N]
       s_pad[i] = (i < 2 * N && (i >= N || p.periodic)) ? sg[i >= N ? i - N : i] : make_float2(0.f, 0.f);
+    if constexpr (CROSS) {
+      const float2* sg2 = p.s2 + (size_t)b * N;
+      for (int i = threadIdx.x; i < NP2X; i += THREADS)
+        s2_pad[i] = (i >= N && i < 2 * N) ? sg2[i - N] : make_float2(0.f, 0.f);
+    }
   }
   if constexpr (GRAD) {
     if constexpr (C::G_SMEM) {
-      for (int i = threadIdx.x; i < S * GS; i += THREADS) gacc_sh[i] = make_float2(0.f, 0.f);
+      for (int i = threadIdx.x; i < NG * S * GS; i += THREADS) gacc_sh[i] = make_float2(0.f, 0.f);
     } else {
       for (int i = threadIdx.x; i < N; i += THREADS) gacc[i] = make_float2(0.f, 0.f);
     }
@@ -490,6 +509,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   if (warp == 0) {
     const double e = warp_energy(sg, N, lane);
     if (lane == 0) red[0] = e;
+  }
+  if constexpr (CROSS) {
+    if (warp == (THREADS > 32 ? 1 : 0)) {
+      if (THREADS <= 32) __syncwarp();
+      const double e2 = warp_energy(p.s2 + (size_t)b * N, N, lane);
+      if (lane == 0) red[1] = e2;
+    }
   }
   Twiddles<C::MX, E2> tw;
   tw.init(t0);
@@ -515,8 +541,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   }
   __syncthreads();
   const double Ed = red[0];
-  const float invE = (float)(1.0 / Ed);
-  const float invE2 = (float)(1.0 / Ed / Ed);
+  // CROSS: normalisation by E1 E2 (reading R25); invE = 1/sqrt(E1 E2) for the surface
+  const double Ed2 = CROSS ? red[1] : Ed;
+  const float invE = CROSS ? (float)(1.0 / sqrt(Ed * Ed2)) : (float)(1.0 / Ed);
+  const float invE2 = (float)(1.0 / Ed / Ed2);
   const float scaleG = p.normalize ? invE2 : 1.0f;
 
   // pass-2 statistics from the combined partials (reading R13)
@@ -592,20 +620,22 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         if (p.periodic && (q < 0 || q >= nrow)) q += (q < 0 ? N : -N);
         return (q >= 0 && q < nrow) ? q : -1;
       };
-      const bool self = (k == 0) || (p.periodic && 2 * k == N);   // row -k is row +k
+      // (CROSS rows are unfolded: every row stands for itself)
+      const bool self = CROSS || (k == 0) || (p.periodic && 2 * k == N);   // row -k is row +k
       const int rowp = wrow(k), rown = self ? -1 : wrow(-k);
       const bool wpos = valid && p.surface && rowp >= 0;
       const bool wneg = valid && p.surface && rown >= 0;
-      lrow = valid && p.loss_on && k <= p.kloss && (k % p.shard_count) == p.shard_index;
+      lrow = valid && p.loss_on &&
+             (CROSS ? (k <= p.kloss && -k <= p.kloss) : (k <= p.kloss && (k % p.shard_count) == p.shard_index));
       const float mult = self ? 1.f : 2.f;
       if constexpr (!SPLIT) {
         const float2* a = sv + t;
-        const float2* c = sv + t - k;
+        const float2* c = sv2 + t - k;
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
       } else {
         const float2* a = sv + 2 * t;
-        const float2* c = sv + 2 * t - k;
+        const float2* c = sv2 + 2 * t - k;
 #pragma unroll
         for (int e = 0; e < E2; ++e) {
           v[e] = cmulc(a[2 * e * T], c[2 * e * T]);
@@ -714,7 +744,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       //      slots: out-of-region slots select 0 (never multiply: exp of an
       //      out-of-region value may overflow).
       if (lrow) {
-        const Mask inm = band & ~(k <= p.ml_k ? mlb : (Mask)0);
+        const Mask inm = band & ~((k < 0 ? -k : k) <= p.ml_k ? mlb : (Mask)0);   // (CROSS rows may be k < 0)
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
         float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f;
         const float gsc = scaleG * mult;
@@ -876,8 +906,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         } else {
           constexpr int CC = E < kCorrChunk ? E : kCorrChunk;
           {
+            // CROSS: term 1 is dL/ds* with the conjugated factor s2[n-k]
             const unsigned g1 = smem_u32(gacc + tb);
-            const float2* s1 = sv + tb - k;
+            const float2* s1 = sv2 + tb - k;
             static_for<0, E / CC>([&](auto c) {
               constexpr int e0 = decltype(c)::value * CC;
               float2 a[CC];
@@ -893,7 +924,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
           sync();
           {
-            const unsigned g2 = smem_u32(gacc + tb - k);
+            // CROSS: term 2 is dL/ds2* (its own accumulator) with s[n]
+            const unsigned g2 = smem_u32((CROSS ? gacc2 : gacc) + tb - k);
             const float2* s2 = sv + tb;
             static_for<0, E / CC>([&](auto c) {
               constexpr int e0 = decltype(c)::value * CC;
@@ -967,6 +999,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       for (int sl = 1; sl < S; ++sl) a = cadd(a, g0[(size_t)sl * GS]);
       gout[n] = a;   // fused: in place over slot 0 (each n is owned by one thread)
     }
+    if constexpr (CROSS) {
+      float2* gout2 = p.gpart2 + ((size_t)b * P + pb) * N;
+      for (int n = threadIdx.x; n < N; n += THREADS) {
+        const float2* g0 = gacc_sh + (size_t)S * GS + n;
+        float2 a = g0[0];
+#pragma unroll 1
+        for (int sl = 1; sl < S; ++sl) a = cadd(a, g0[(size_t)sl * GS]);
+        gout2[n] = a;
+      }
+    }
   }
 
   // ---- fused finalize over the cluster (SURVEY §8(a) a4 + a7 final, K5)
@@ -1008,6 +1050,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   }
 }
 
+#ifdef GRAF_API_UNIT   // the reductions and small kernels live in the ABI unit only
 // zero-padded copy of s for the global-memory path: s_pad[b][i] = s[b][i - N] for
 // i in [N, 2N), 0 elsewhere in [0, N + M)
 __global__ void pad_s_kernel(const float2* s, float2* s_pad, int N, int M, long long B, int periodic) {
@@ -1085,17 +1128,25 @@ struct FinalizeParams {
   float lam_match;
   double* loss;                  // may be NULL
   float2* grad;                  // may be NULL
+  // cross-ambiguity: the second waveform, its partial gradients and output (else NULL)
+  const float2* s2;
+  const float2* gpart2;
+  float2* grad2;
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   const int b = blockIdx.x;
   const int N = f.N;
   const float2* sg = f.s + (size_t)b * N;
-  __shared__ double sh[2];
+  const float2* sg2 = f.s2 ? f.s2 + (size_t)b * N : nullptr;
+  __shared__ double sh[3];
   if (threadIdx.x < 32) {
     const double e = warp_energy(sg, N, threadIdx.x);
+    // cross-ambiguity: E1 E2 replaces E^2 (reading R25)
+    const double e2 = sg2 ? warp_energy(sg2, N, threadIdx.x) : e;
     if (threadIdx.x == 0) {
       sh[0] = e;
+      sh[2] = e2;
       double S = 0, Z = 0, F = 0, Mt = 0;
       double m = -INFINITY;
       for (int q = 0; q < f.P; ++q) {
@@ -1113,7 +1164,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
           mg = f.global[b].lse_max;
           Zg = f.global[b].lse_sum;
         }
-        double L = f.lam_isl * (f.normalize ? Sg / (e * e) : Sg);
+        double L = f.lam_isl * (f.normalize ? Sg / (e * e2) : Sg);
         if (f.lam_psl != 0.f) L += f.lam_psl * (mg + (double)f.T * log(Zg));
         if (f.lam_match != 0.f) L += f.lam_match * Mt;
         f.loss[b] = L;
@@ -1122,8 +1173,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   }
   __syncthreads();
   if (!f.grad) return;
-  const double E = sh[0];
-  const float coef = (f.grad_norm_term && f.normalize) ? (float)(2.0 * sh[1] / (E * E * E)) : 0.f;
+  const double E = sh[0], E2 = sh[2];
+  const bool nt = f.grad_norm_term && f.normalize;
+  // auto: -(2/E^3) F s;  cross: -F/(E1^2 E2) s1 and -F/(E1 E2^2) s2
+  const float coef = nt ? (float)((sg2 ? 1.0 : 2.0) * sh[1] / (E * E * E2)) : 0.f;
+  const float coef2 = nt ? (float)(sh[1] / (E * E2 * E2)) : 0.f;
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
     double gx = 0, gy = 0;
     for (int q = 0; q < f.P; ++q) {
@@ -1133,6 +1187,16 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
     }
     const float2 sv = sg[n];
     f.grad[(size_t)b * N + n] = make_float2((float)gx - coef * sv.x, (float)gy - coef * sv.y);
+    if (sg2) {
+      double hx = 0, hy = 0;
+      for (int q = 0; q < f.P; ++q) {
+        const float2 a = f.gpart2[((size_t)b * f.P + q) * N + n];
+        hx += a.x;
+        hy += a.y;
+      }
+      const float2 s2v = sg2[n];
+      f.grad2[(size_t)b * N + n] = make_float2((float)hx - coef2 * s2v.x, (float)hy - coef2 * s2v.y);
+    }
   }
 }
 
@@ -1457,5 +1521,7 @@ __global__ void __launch_bounds__(256) phase_adam_kernel(AdamParams a) {
   __syncthreads();
   if (threadIdx.x == 0) a.step[b] = t;
 }
+
+#endif  // GRAF_API_UNIT
 
 }  // namespace graf

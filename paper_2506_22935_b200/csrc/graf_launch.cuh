@@ -1,0 +1,207 @@
+// graf_launch.cuh — launch planning shared by the ABI translation unit
+// (graf_api.cu) and the per-size row-kernel translation units (graf_rows_*.cu,
+// compiled in parallel; each instantiates af_rows_kernel for its sizes).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "../../include/graf.h"
+#include "graf_kernels.cuh"
+
+namespace graf {
+
+extern thread_local int t_launches;   // kernels / memsets enqueued by the current entry-point call
+constexpr int kMaxDev = 64;
+constexpr int kNumSM = 148;  // B200; the plan is a pure function of the descriptors
+
+// ---------------------------------------------------------------------------
+// launch plan
+// ---------------------------------------------------------------------------
+struct Plan {
+  int M = 0, threads = 0, S = 0, T = 0, P = 1, Pbound = 1;
+  int U = 0, row_lo = 0, row_step = 1;
+  bool fixedP = false;
+  bool s_smem = true, g_smem = true;
+  size_t smem = 0;
+  // surface staging for bulk async row stores: per-slot floats,
+  // whether the rows qualify, and whether they fit the slot's exchange buffer (alias)
+  int stg_floats = 0;
+  bool bulk_ok = false, alias_ok = false;
+  size_t smem_stg = 0;
+  int bulk_mode = -1;   // decided at the first launch of a call: 0 direct, 1 dedicated, 2 alias
+  // left-padded gradient accumulators (M == N loss calls), if they cost no resident CTA
+  bool gpad_ok = false;
+  size_t smem_gpad = 0;
+  int gpad_mode = -1;
+  // fused finalize (K_ISL only): requested by the caller, granted when P <= 8
+  bool fuse_req = false, fused = false;
+  bool cross = false;   // cross-ambiguity (two waveforms, unfolded rows)
+  size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
+};
+
+
+// Cost model: waves x (row iterations + CTA setup), setup ~ one row iteration.
+inline int choose_P(const Plan& pl, long long B, int occ, int nsm) {
+  const long long cap = (long long)nsm * std::max(occ, 1);
+  int best = 1;
+  double best_t = 1e300;
+  for (int P = 1; P <= pl.Pbound; ++P) {
+    const long long ctas = (long long)P * B;
+    const double waves = (double)((ctas + cap - 1) / cap);
+    const double iters = (double)((pl.U + (long long)P * pl.S - 1) / ((long long)P * pl.S));
+    const double t = waves * (iters + 1.0);
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = P;
+    }
+  }
+  return best;
+}
+
+template <int M, int KIND, bool WGT, bool CROSS = false>
+cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
+  static std::once_flag once[kMaxDev];
+  static cudaError_t attr_err[kMaxDev];
+  static int sm_count[kMaxDev];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::call_once(once[dev], [dev] {
+    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M, KIND, WGT, CROSS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (attr_err[dev] == cudaSuccess)
+      attr_err[dev] = cudaDeviceGetAttribute(&sm_count[dev], cudaDevAttrMultiProcessorCount, dev);
+  });
+  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
+  *nsm = sm_count[dev];
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT, CROSS>, Cfg<M>::THREADS,
+                                                       smem);
+}
+
+template <int M, int KIND, bool WGT, bool CROSS = false>
+cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
+  int occ = 1, nsm = kNumSM;
+  // (also sets the instantiation's large-shared-memory attribute, once per device)
+  cudaError_t e0 = kernel_occupancy<M, KIND, WGT, CROSS>(pl.smem, &occ, &nsm);
+  if (e0 != cudaSuccess) return e0;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  size_t smem = pl.smem;
+  rp.gpad = 0;
+  if (pl.gpad_ok && KIND != K_ADJ && KIND != K_FWD && KIND != K_FWDA) {
+    if (pl.gpad_mode < 0) {
+      int occ_g = 0;
+      const bool fits = pl.smem + pl.smem_gpad <= 227 * 1024;
+      if (fits) {
+        e0 = kernel_occupancy<M, KIND, WGT, CROSS>(pl.smem + pl.smem_gpad, &occ_g, &nsm);
+        if (e0 != cudaSuccess) return e0;
+      }
+      pl.gpad_mode = (fits && occ_g >= occ) ? 1 : 0;
+    }
+    if (pl.gpad_mode == 1) {
+      rp.gpad = 1;
+      smem += pl.smem_gpad;
+    }
+  }
+  if (rp.surface && pl.bulk_ok) {
+    if (pl.bulk_mode < 0) {
+      // dedicated staging unless it costs resident CTAs and the exchange buffer can hold the rows
+      int occ_d = 0;
+      const bool fits = smem + pl.smem_stg <= 227 * 1024;
+      if (fits) {
+        e0 = kernel_occupancy<M, KIND, WGT, CROSS>(smem + pl.smem_stg, &occ_d, &nsm);
+        if (e0 != cudaSuccess) return e0;
+      }
+      pl.bulk_mode = (fits && (occ_d >= occ || !pl.alias_ok) && occ_d >= 1) ? 1 : pl.alias_ok ? 2 : 0;
+    }
+    rp.bulk = pl.bulk_mode;
+    rp.stg_floats = pl.stg_floats;
+    if (rp.bulk == 1) {
+      smem += pl.smem_stg;
+      e0 = kernel_occupancy<M, KIND, WGT, CROSS>(smem, &occ, &nsm);
+      if (e0 != cudaSuccess) return e0;
+    }
+  } else {
+    rp.bulk = 0;
+  }
+  if (!pl.fixedP) {
+    pl.P = choose_P(pl, B, occ, nsm);
+    pl.fixedP = true;   // later passes of the same call reuse it
+  }
+  rp.fuse = 0;
+  if (KIND == K_ISL && !CROSS && pl.fuse_req && pl.P >= 2 && pl.P <= 8) {   // (P = 1: measured slower as a cluster launch)
+    rp.fuse = 1;
+    pl.fused = true;
+  }
+  for (int b0 = 0; b0 < B; b0 += 65535) {
+    rp.b0 = b0;
+    dim3 grid(pl.P, std::min(65535, B - b0));
+    rp.smem_bytes = (int)smem;
+    if (rp.fuse) {
+      // the P CTAs of a waveform form one thread-block cluster (rank 0 finalizes)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(pl.threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)pl.P;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, af_rows_kernel<M, KIND, WGT, CROSS>, rp);
+      if (e != cudaSuccess) return e;
+    } else {
+      af_rows_kernel<M, KIND, WGT, CROSS><<<grid, pl.threads, smem, st>>>(rp);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ++t_launches;
+  }
+  return cudaSuccess;
+}
+
+template <int M>
+cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind, bool wgt) {
+  if (pl.cross) {
+    // cross-ambiguity kernels: unweighted, M <= 4096 (the second waveform is staged too)
+    if constexpr (M <= 4096) {
+      switch (kind) {
+        case K_FWD: return launch_kernel<M, K_FWD, false, true>(pl, rp, B, st);
+        case K_ISL: return launch_kernel<M, K_ISL, false, true>(pl, rp, B, st);
+        case K_PASS2: return launch_kernel<M, K_PASS2, false, true>(pl, rp, B, st);
+        case K_ADJ: return launch_kernel<M, K_ADJ, false, true>(pl, rp, B, st);
+        default: return cudaErrorNotSupported;
+      }
+    } else {
+      return cudaErrorNotSupported;
+    }
+  }
+  switch (kind) {
+    case K_FWD:
+      if (rp.want_argmax)
+        return wgt ? launch_kernel<M, K_FWDA, true>(pl, rp, B, st) : launch_kernel<M, K_FWDA, false>(pl, rp, B, st);
+      return wgt ? launch_kernel<M, K_FWD, true>(pl, rp, B, st) : launch_kernel<M, K_FWD, false>(pl, rp, B, st);
+    case K_ISL: return wgt ? launch_kernel<M, K_ISL, true>(pl, rp, B, st) : launch_kernel<M, K_ISL, false>(pl, rp, B, st);
+    case K_PASS2:
+      return wgt ? launch_kernel<M, K_PASS2, true>(pl, rp, B, st) : launch_kernel<M, K_PASS2, false>(pl, rp, B, st);
+    case K_ADJ: return launch_kernel<M, K_ADJ, false>(pl, rp, B, st);
+    case K_MATCH:
+      return wgt ? launch_kernel<M, K_MATCH, true>(pl, rp, B, st) : launch_kernel<M, K_MATCH, false>(pl, rp, B, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+
+// one instantiation per size, defined in graf_rows_*.cu
+template <int M>
+cudaError_t launch_rows_size(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind);
+// upload of the twiddle table into one translation unit's copy
+using TwUpload = cudaError_t (*)(const float2*);
+std::vector<TwUpload>& tw_uploaders();
+
+}  // namespace graf

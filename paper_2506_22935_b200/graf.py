@@ -340,3 +340,64 @@ class LpiOptimizer:
                 self._iteration()
         self.stream.synchronize()
         return self.loss
+
+
+# ---------------------------------------------------------------------------
+# Cross-ambiguity X[k,m] = sum_n s1[n] conj(s2[n-k]) W^{mn}
+# ---------------------------------------------------------------------------
+def xaf_forward(s1: torch.Tensor, s2: torch.Tensor, M: int, *, out: Optional[str] = "c64",
+                layout: str = "centered", k_begin=None, k_end=None, normalize_output: bool = False,
+                loss: Optional[LossSpec] = None, ws: Optional[Workspace] = None, surface=None, stream=None):
+    """graf_xaf_forward: cross surface window and/or loss partials."""
+    s1, s2 = _check_s(s1), _check_s(s2)
+    assert s1.shape == s2.shape
+    d = _desc(s1, M, out, layout, k_begin, k_end, normalize_output)
+    ld = loss.desc() if loss is not None else None
+    if surface is None:
+        surface = _surface_alloc(d, s1.device)
+    partials = torch.empty((s1.shape[0], NPART), dtype=torch.float64, device=s1.device) if loss is not None else None
+    nbytes = int(L.lib().graf_xaf_workspace_bytes(ctypes.byref(d), ctypes.byref(ld) if ld else None))
+    wp, wn = (ws or _ws).get(nbytes, s1.device)
+    L.check(L.lib().graf_xaf_forward(ctypes.byref(d), ctypes.byref(ld) if ld else None,
+                                     ctypes.c_void_p(s1.data_ptr()), ctypes.c_void_p(s2.data_ptr()), _ptr(surface),
+                                     _ptr(partials), ctypes.c_void_p(wp), wn, _stream(stream)))
+    return surface, partials
+
+
+def xaf_loss_grad(s1: torch.Tensor, s2: torch.Tensor, M: int, loss: LossSpec, *, out: Optional[str] = None,
+                  layout: str = "centered", k_begin=None, k_end=None, ws: Optional[Workspace] = None,
+                  surface=None, stream=None):
+    """graf_xaf_loss_grad -> (loss[B] float64, dL/ds1* [B,N], dL/ds2* [B,N], surface or None)."""
+    s1, s2 = _check_s(s1), _check_s(s2)
+    assert s1.shape == s2.shape
+    d = _desc(s1, M, out, layout, k_begin, k_end)
+    ld = loss.desc()
+    B, N = s1.shape
+    g1 = torch.empty((B, N), dtype=torch.complex64, device=s1.device)
+    g2 = torch.empty_like(g1)
+    lo = torch.empty((B,), dtype=torch.float64, device=s1.device)
+    if surface is None:
+        surface = _surface_alloc(d, s1.device)
+    nbytes = int(L.lib().graf_xaf_workspace_bytes(ctypes.byref(d), ctypes.byref(ld)))
+    wp, wn = (ws or _ws).get(nbytes, s1.device)
+    L.check(L.lib().graf_xaf_loss_grad(ctypes.byref(d), ctypes.byref(ld), ctypes.c_void_p(s1.data_ptr()),
+                                       ctypes.c_void_p(s2.data_ptr()), None, _ptr(lo), _ptr(g1), _ptr(g2),
+                                       _ptr(surface), ctypes.c_void_p(wp), wn, _stream(stream)))
+    return lo, g1, g2, surface
+
+
+def xaf_backward(s1: torch.Tensor, s2: torch.Tensor, M: int, dA: torch.Tensor, *, k_begin=None, k_end=None,
+                 layout: str = "centered", ws: Optional[Workspace] = None, stream=None):
+    """graf_xaf_backward: (dL/ds1*, dL/ds2*) from dA = dL/dX* over rows [k_begin, k_end)."""
+    s1, s2 = _check_s(s1), _check_s(s2)
+    dA = dA.contiguous()
+    d = _desc(s1, M, None, layout, k_begin, k_end)
+    B, N = s1.shape
+    g1 = torch.empty((B, N), dtype=torch.complex64, device=s1.device)
+    g2 = torch.empty_like(g1)
+    nbytes = int(L.lib().graf_xaf_workspace_bytes(ctypes.byref(d), None))
+    wp, wn = (ws or _ws).get(nbytes, s1.device)
+    L.check(L.lib().graf_xaf_backward(ctypes.byref(d), ctypes.c_void_p(s1.data_ptr()),
+                                      ctypes.c_void_p(s2.data_ptr()), ctypes.c_void_p(dA.data_ptr()), _ptr(g1),
+                                      _ptr(g2), ctypes.c_void_p(wp), wn, _stream(stream)))
+    return g1, g2

@@ -24,16 +24,16 @@ def build(cfg, specs):
     from paper_2506_22935_b200 import _build
     M = CONFIGS[cfg]["M"]
     os.makedirs(VDIR, exist_ok=True)
-    procs = []
+    srcs = [os.path.join(_build.CSRC, "graf_api.cu"), os.path.join(_build.CSRC, _build.ROW_UNIT_OF[M])]
     for spec in specs:
         tag, defs = spec.split(":", 1)
         out = os.path.join(VDIR, f"libgraf_c{cfg}_{tag}.so")
-        cmd = [_build.nvcc(), *_build.NVCC_FLAGS, f"-DGRAF_ONLY_M={M}"]
-        cmd += [f"-D{d}" for d in defs.split(",") if d]
-        cmd += ["-o", out, *_build.SOURCES]
-        procs.append((tag, subprocess.Popen(cmd, cwd=_build.CSRC)))
-    for tag, p in procs:
-        print(tag, "rc", p.wait())
+        try:
+            _build.compile_link(out, srcs, defines=[f"GRAF_ONLY_M={M}"] + [d for d in defs.split(",") if d],
+                                objdir=os.path.join(VDIR, "obj_" + tag))
+            print(tag, "rc 0")
+        except Exception as e:   # noqa: BLE001
+            print(tag, "failed", e)
 
 
 def one(lib, cfg, steps=30):
