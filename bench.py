@@ -147,6 +147,9 @@ def cpu_baseline(w: dict, budget_s: float = 12.0) -> dict:
         elif w.get("match"):
             tgt = np.random.default_rng(b).random((2 * N - 1, M)) / M
             O.match_loss_and_grad(s, M, spec, tgt, -(N - 1), "centered")
+        elif w.get("cross"):
+            s2 = config_waveforms(w["cid"], batch=1, start=(b + 777) % w["B"])[0]
+            O.cross_loss_and_grad(s, s2, M, spec)
         else:
             per = w.get("periodic", False)
             O.loss_and_grad(s, M, spec, periodic=per)
@@ -182,6 +185,10 @@ def run_reference(args, w) -> None:
             if w.get("match"):
                 tgt = np.random.default_rng(j).random((2 * w["N"] - 1, w["M"])) / w["M"]
                 O.match_loss_and_grad(s, w["M"], spec, tgt, -(w["N"] - 1), "centered")
+                continue
+            if w.get("cross"):
+                s2 = config_waveforms(w["cid"], batch=1, start=(j + 777) % w["B"])[0]
+                O.cross_loss_and_grad(s, s2, w["M"], spec)
                 continue
             O.loss_and_grad(s, w["M"], spec, periodic=per)
             if w["cfg"]["surface"]:
@@ -221,7 +228,7 @@ def main():
     ap.add_argument("--impl", default="graf", choices=["graf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0)
-    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward", "lpi", "match"],
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward", "lpi", "match", "cross"],
                     help="forward: full-surface mode (graf_af_forward writes the config's surface, no loss)")
     ap.add_argument("--periodic", action="store_true",
                     help="the paper's circular surface (Eq. 2 / Alg. 1, SURVEY 8(f) NEXT-1); needs M == N")
@@ -259,6 +266,14 @@ def main():
         w["surf_bytes"] = w["B"] * (2 * w["rows"] - 1) * min(w["M"], 2 * w["loss"]["d_max"] + 1) * 4
         w["launches"] = 2
         w["note"] = "match loss over the region, per-waveform fp32 target of the surface window (HBM-streamed)"
+    if args.mode == "cross":
+        # cross-ambiguity of waveform pairs (NEXT-4): the config's loss on
+        # X = sum s1 conj(s2(n-k)) W^{mn}, rows unfolded (no mirror symmetry)
+        w["cross"] = True
+        w["rows"] = 2 * min(w["loss"]["k_max"], w["N"] - 1) + 1
+        w["flops"] = w["B"] * w["rows"] * w["ffts"] * 5.0 * w["M"] * math.log2(w["M"])
+        w["io_bytes"] = w["B"] * w["N"] * 8 * 4
+        w["note"] = "cross-ambiguity of (s1, s2) pairs, unfolded rows; loss/grad w.r.t. both"
     if args.impl == "reference":
         return run_reference(args, w)
 
@@ -307,7 +322,14 @@ def main():
         s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=0)).pin_memory()
         s = s_host.to(dev)
 
+    if w.get("cross"):
+        s2_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=rank * B + 777)).pin_memory()
+        s2 = s2_host.to(dev)
+
     def call(st=None):
+        if w.get("cross"):
+            graf.xaf_loss_grad(s, s2, M, spec, ws=ws, stream=st)
+            return
         if delay:
             sharding.delay_sharded_loss_grad(s, M, spec, backend=tb)
             return
@@ -413,7 +435,9 @@ def main():
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             s_dev2.copy_(s_host, non_blocking=True)
-            if delay:
+            if w.get("cross"):
+                lo, gr, gr2, _ = graf.xaf_loss_grad(s_dev2, s2, M, spec, ws=ws, stream=stream)
+            elif delay:
                 lo, gr = sharding.delay_sharded_loss_grad(s_dev2, M, spec)
             elif args.mode == "forward":
                 sf, _ = graf.af_forward(s_dev2, M, out=out, layout="centered", ws=ws, surface=surf, stream=stream,

@@ -20,3 +20,5 @@ python -c "
 import json
 for c in ('c2match','c3match'):
     d=json.load(open('gpurun_out/bench_${TAG}_'+c+'.json')); r=d['roofline']; print(c, d['ms_per_step'], r['bound'], r['frac'])"
+timeout 600 python bench.py --config 2 --mode cross --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c2cross.json 2> gpurun_out/bench_${TAG}_c2cross.err
+python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c2cross.json')); r=d['roofline']; print('c2cross', d['ms_per_step'], r['bound'], r['frac'])"
