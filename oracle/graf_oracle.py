@@ -54,7 +54,7 @@ __all__ = [
     "loss_and_grad", "adjoint", "correlate", "surface", "loss_and_grad_chunked",
     "periodic_ambiguity", "hard_psl_and_grad", "spectral_variance_and_grad", "phase_grad",
     "adam_step", "lpi_loss_and_grad", "match_loss_and_grad", "cross_lag_products", "cross_ambiguity",
-    "cross_correlate", "cross_adjoint", "cross_loss_and_grad",
+    "cross_correlate", "cross_adjoint", "cross_loss_and_grad", "mainlobe_width_and_grad",
 ]
 
 
@@ -550,3 +550,29 @@ def cross_loss_and_grad(s1, s2, M: int, spec: LossSpec):
         g1 = g1 - F / (E1 ** 2 * E2) * s1
         g2 = g2 - F / (E1 * E2 ** 2) * s2
     return L, g1, g2
+
+
+# ---------------------------------------------------------------------------
+# Mainlobe width: the -3 dB delay width through
+# the differentiable sigmoid threshold
+#   W = sum_tau |tau| * sigma(gamma * (chi(tau, 0) - 0.5 chi(0, 0)))
+# over every delay of the zero-Doppler cut (aperiodic tau in +-(N-1), or the
+# periodic residues in (-N/2, N/2]), chi raw (reading R26).
+# ---------------------------------------------------------------------------
+def mainlobe_width_and_grad(s: np.ndarray, gamma: float, periodic: bool = False):
+    """(W, dW/ds*) with dW/dchi(tau,0) = |tau| gamma sigma'(u) and the chi(0,0) = E^2 term."""
+    s = np.asarray(s, dtype=np.complex128)
+    n = s.shape[0]
+    rows = delay_rows(n, periodic=periodic)
+    A = ambiguity(s, n if periodic else max(2, n), rows=rows, bins=np.array([0]), periodic=periodic)[:, 0]
+    chi = A.real ** 2 + A.imag ** 2
+    E = energy(s)
+    u = gamma * (chi - 0.5 * E ** 2)
+    sig = 0.5 * (1.0 + np.tanh(0.5 * u))                # logistic sigma, overflow-free
+    W = float(np.sum(np.abs(rows) * sig))
+    dsig = sig * (1.0 - sig)
+    c = np.abs(rows) * gamma * dsig                     # dW/dchi(tau, 0)
+    G = (c * A)[:, None]                                # dW/dA*(tau, 0) = c * A
+    g = adjoint(s, n if periodic else max(2, n), G, rows, np.array([0]), periodic)
+    g = g - 0.5 * float(np.sum(c)) * 2.0 * E * s        # through chi(0,0) = E^2: d(E^2)/ds* = 2 E s
+    return W, g

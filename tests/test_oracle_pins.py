@@ -585,3 +585,25 @@ def test_cross_adjoint_inner_product_identity():
     lin = (O.cross_ambiguity(s1 + d1, s2 + d2, M) - O.cross_ambiguity(s1 - d1, s2 - d2, M)) / 2
     g1, g2 = O.cross_adjoint(s1, s2, M, G, rows)
     assert abs(np.vdot(G, lin).real - (np.vdot(g1, d1).real + np.vdot(g2, d2).real)) < 1e-10
+
+
+# ---------------------------------------------------------------- mainlobe width (NEXT-3)
+@pytest.mark.parametrize("periodic", [False, True])
+def test_mainlobe_width_pins(periodic):
+    n = 8
+    s = rs(n, 140)
+    E = O.energy(s)
+    W, g = O.mainlobe_width_and_grad(s, gamma=0.3 / E ** 2, periodic=periodic)
+    fd = _fd(lambda z: O.mainlobe_width_and_grad(z, 0.3 / E ** 2, periodic)[0], s)
+    np.testing.assert_allclose(2 * g, fd, atol=1e-7 * max(1.0, np.abs(fd).max()))
+    # gamma -> infinity: the hard -3 dB count sum_{chi(tau,0) > E^2/2} |tau|
+    rows = O.delay_rows(n, periodic=periodic)
+    cut = np.abs(O.ambiguity(s, n, rows=rows, bins=np.array([0]), periodic=periodic)[:, 0]) ** 2
+    hard = float(np.sum(np.abs(rows)[cut > 0.5 * E ** 2]))
+    Wh, _ = O.mainlobe_width_and_grad(s, gamma=1e6 / E ** 2, periodic=periodic)
+    assert abs(Wh - hard) < 1e-6
+    # constant pulse: chi(tau,0) = (N-|tau|)^2 > N^2/2 iff |tau| < N(1 - 1/sqrt 2)
+    one = np.ones(16, complex)
+    Wc, gc = O.mainlobe_width_and_grad(one, gamma=1e3, periodic=False)
+    t = np.arange(-15, 16)
+    assert abs(Wc - float(np.sum(np.abs(t)[(16 - np.abs(t)) ** 2 > 128]))) < 1e-9
