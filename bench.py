@@ -228,13 +228,15 @@ def main():
     ap.add_argument("--impl", default="graf", choices=["graf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0)
-    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward", "lpi", "match", "cross"],
+    ap.add_argument("--mode", default="loss_grad", choices=["loss_grad", "forward", "lpi", "match", "cross", "mlw"],
                     help="forward: full-surface mode (graf_af_forward writes the config's surface, no loss)")
     ap.add_argument("--periodic", action="store_true",
                     help="the paper's circular surface (Eq. 2 / Alg. 1, SURVEY 8(f) NEXT-1); needs M == N")
     args = ap.parse_args()
     if args.mode == "lpi":
         return run_lpi(args)
+    if args.mode == "mlw":
+        return run_mlw(args)
     w = workload(args.config)
     w["periodic"] = bool(args.periodic)
     if args.periodic:
@@ -595,6 +597,46 @@ def run_lpi(args):
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_mlw(args):
+    """Differentiable mainlobe width W = sum |tau| sigma(gamma (chi(tau,0) - chi(0,0)/2)) and
+    its gradient on the c2 batch (B = 256, N = 256): a step = one
+    graf_mainlobe_width call (O(N^2) direct zero-Doppler cut per waveform)."""
+    import torch
+    import paper_2506_22935_b200 as graf
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    B, N = 256, 256
+    s = torch.from_numpy(config_waveforms(2, batch=B)).to(dev)
+    loss = torch.empty(B, dtype=torch.float64, device=dev)
+    grad = torch.empty((B, N), dtype=torch.complex64, device=dev)
+    gam = 4.0 / float(N) ** 2
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        graf.mainlobe_width(s, gam, loss=loss, grad=grad, stream=st)
+        g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        graf.mainlobe_width(s, gam, loss=loss, grad=grad, stream=st)
+    W = max(3, args.warmup)
+    with torch.cuda.stream(st):
+        for _ in range(W):
+            g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        a.record(st)
+        for _ in range(args.steps):
+            g.replay()
+        b.record(st)
+    b.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    print(json.dumps({"metric": "mainlobe-width loss+grad surfaces/sec", "value": B / (ms / 1e3),
+                      "unit": "surfaces/s", "n_gpus": 1, "steps": args.steps, "warmup": W, "ms_per_step": ms,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                      "data": "synthetic", "config": {"workload": "c2 batch, W over the zero-Doppler cut, "
+                                                                  "gamma = 4/N^2", "B": B, "N": N},
+                      "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": args.steps}))
 
 
 class TimedBackend:

@@ -197,6 +197,15 @@ graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, floa
                                    const float* weights, double* loss, void* grad, int32_t accumulate,
                                    void* stream);
 
+/* Differentiable mainlobe width:
+ *   W_b = sum_tau |tau| sigma(gamma (chi(tau,0) - chi(0,0)/2))
+ * over every delay of the zero-Doppler cut (aperiodic tau in +-(N-1), periodic = 1:
+ * the residues of (-N/2, N/2]), chi raw (reading R26), and dW/ds*.  Writes (or with
+ * accumulate = 1 adds) weight*W_b into loss[b] and weight*dW/ds* into grad[b][:].
+ * s, grad: complex64 [B][N]; 1 <= N <= 8192 (v1); no workspace. */
+graf_status graf_mainlobe_width(int64_t batch, int32_t n, const void* s, float gamma, float weight,
+                                int32_t periodic, double* loss, void* grad, int32_t accumulate, void* stream);
+
 /* One Adam step (L425: Adam, learning rate 0.01) on the phases of phase-coded
  * waveforms s = exp(j*theta):  dL/dtheta = -2 Im(s conj(g)) from g = dL/ds*
  * (complex64 [B][N]); m, v: float [B][N] moments; step: int32 [B] completed steps

@@ -8,8 +8,8 @@ Public API (thin binding of include/graf.h; all compute in libgraf.so):
 from ._lib import GrafError, lib  # noqa: F401
 from .graf import (AF, AFLoss, LossSpec, LpiOptimizer, af, af_backward, af_forward, af_loss,  # noqa: F401
                    af_loss_grad, combine_partials, phase_adam_step, spectral_variance, workspace_bytes,
-                   xaf_backward, xaf_forward, xaf_loss_grad)
+                   mainlobe_width, xaf_backward, xaf_forward, xaf_loss_grad)
 
 __all__ = ["AF", "AFLoss", "LossSpec", "af", "af_backward", "af_forward", "af_loss", "af_loss_grad",
            "combine_partials", "workspace_bytes", "GrafError", "lib", "spectral_variance", "phase_adam_step",
-           "LpiOptimizer", "xaf_forward", "xaf_loss_grad", "xaf_backward"]
+           "LpiOptimizer", "xaf_forward", "xaf_loss_grad", "xaf_backward", "mainlobe_width"]

@@ -19,7 +19,7 @@ EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_wo
            "graf_af_forward", "graf_af_loss_grad", "graf_af_backward", "graf_combine_partials",
            "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
            "graf_phase_adam_step", "graf_xaf_workspace_bytes", "graf_xaf_forward", "graf_xaf_loss_grad",
-           "graf_xaf_backward")
+           "graf_xaf_backward", "graf_mainlobe_width")
 
 
 class AfDesc(ctypes.Structure):
@@ -88,6 +88,9 @@ def lib() -> ctypes.CDLL:
         L.graf_xaf_backward.restype = c_int32
         L.graf_xaf_backward.argtypes = [POINTER(AfDesc), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_size_t, c_void_p]
+        L.graf_mainlobe_width.restype = c_int32
+        L.graf_mainlobe_width.argtypes = [c_int64, c_int32, c_void_p, c_float, c_float, c_int32, c_void_p, c_void_p,
+                                          c_int32, c_void_p]
         L.graf_spectral_variance.restype = c_int32
         L.graf_spectral_variance.argtypes = [c_int64, c_int32, c_void_p, c_float, c_void_p, c_void_p, c_void_p,
                                              c_int32, c_void_p]

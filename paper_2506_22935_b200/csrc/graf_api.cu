@@ -838,6 +838,30 @@ graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, floa
   return GRAF_OK;
 }
 
+graf_status graf_mainlobe_width(int64_t batch, int32_t n, const void* s, float gamma, float weight,
+                                int32_t periodic, double* loss, void* grad, int32_t accumulate, void* stream) {
+  t_launches = 0;
+  if (batch < 1 || batch > (1LL << 31) - 1 || n < 1) return fail(GRAF_EINVAL, "batch / N out of range");
+  if (n > 8192) return fail(GRAF_EUNSUPPORTED, "mainlobe width: N = %d > 8192 (v1)", n);
+  if (periodic && !is_pow2(n)) return fail(GRAF_EINVAL, "periodic mainlobe width needs N a power of two");
+  if (!s || !grad || !aligned8(s) || !aligned8(grad)) return fail(GRAF_EINVAL, "s / grad NULL or misaligned");
+  if (!std::isfinite(gamma) || !std::isfinite(weight)) return fail(GRAF_EINVAL, "non-finite gamma / weight");
+  MlwParams q{static_cast<const float2*>(s), n, periodic ? 1 : 0, accumulate ? 1 : 0, gamma, weight, loss,
+              static_cast<float2*>(grad)};
+  const int K = periodic ? n / 2 : n - 1;
+  int threads = 32;
+  while (threads < 1024 && threads < n) threads *= 2;
+  const size_t smem = sizeof(float2) * (size_t)(K + 1) + sizeof(float) * (size_t)((K + 2) & ~1) +
+                      sizeof(double) * threads;
+  cudaError_t e = cudaFuncSetAttribute(mainlobe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "mainlobe_kernel attribute");
+  mainlobe_kernel<<<(unsigned)batch, threads, smem, static_cast<cudaStream_t>(stream)>>>(q);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "mainlobe_kernel launch");
+  ++t_launches;
+  return GRAF_OK;
+}
+
 graf_status graf_phase_adam_step(int64_t batch, int32_t n, float* theta, float* m, float* v, int32_t* step,
                                  const void* grad, void* s_out, float lr, float beta1, float beta2, float eps,
                                  void* stream) {

@@ -1522,6 +1522,95 @@ __global__ void __launch_bounds__(256) phase_adam_kernel(AdamParams a) {
   if (threadIdx.x == 0) a.step[b] = t;
 }
 
+// ---------------------------------------------------------------------------
+// Mainlobe width (reading R26):
+//   W = sum_tau |tau| sigma(gamma (chi(tau,0) - E^2/2)),  chi(tau,0) = |A_tau|^2,
+//   A_tau = sum_n s[n] conj(s[n - tau]) (the zero-Doppler cut; A_{-tau} = conj A_tau),
+//   dW/ds*[p] = sum_tau c_tau (A_tau s[p-tau] + conj(A_tau) s[p+tau]) - (sum_tau c_tau) E s[p],
+//   c_tau = |tau| gamma sigma'(u_tau).
+// One CTA per waveform, O(N^2) direct sums (the cut is one Doppler bin of every
+// delay row); A_tau for tau >= 0 kept in shared memory.
+// ---------------------------------------------------------------------------
+struct MlwParams {
+  const float2* s;
+  int N, periodic, accumulate;
+  float gamma, weight;
+  double* loss;
+  float2* grad;
+};
+
+__global__ void __launch_bounds__(1024) mainlobe_kernel(MlwParams q) {
+  extern __shared__ float4 smem_raw[];
+  const int N = q.N, b = blockIdx.x, t = threadIdx.x;
+  const int K = q.periodic ? N / 2 : N - 1;            // taus 0..K (mirrors implied)
+  float2* At = reinterpret_cast<float2*>(smem_raw);     // [K + 1]
+  float* ct = reinterpret_cast<float*>(At + K + 1);     // [K + 1] c_tau * mult
+  double* buf = reinterpret_cast<double*>(ct + ((K + 2) & ~1));   // [blockDim]
+  const float2* sg = q.s + (size_t)b * N;
+  double E = 0.0;
+  for (int n = t; n < N; n += blockDim.x) E += (double)sg[n].x * sg[n].x + (double)sg[n].y * sg[n].y;
+  E = cta_tree_sum(E, buf);
+  const double halfE2 = 0.5 * E * E;
+  double Wsum = 0.0, Csum = 0.0;
+  for (int tau = t; tau <= K; tau += blockDim.x) {
+    float ax = 0.f, ay = 0.f;
+    for (int n = 0; n < N; ++n) {
+      int j = n - tau;
+      if (q.periodic) j = j < 0 ? j + N : j;
+      else if (j < 0) continue;
+      const float2 r = cmulc(sg[n], sg[j]);
+      ax += r.x;
+      ay += r.y;
+    }
+    At[tau] = make_float2(ax, ay);
+    const bool self = (tau == 0) || (q.periodic && 2 * tau == N);
+    const float mult = self ? 1.f : 2.f;
+    const double chi = (double)ax * ax + (double)ay * ay;
+    const double u = (double)q.gamma * (chi - halfE2);
+    const double sig = 0.5 * (1.0 + tanh(0.5 * u));
+    Wsum += mult * tau * sig;
+    const double c = (double)tau * q.gamma * sig * (1.0 - sig);
+    ct[tau] = (float)(mult * c);
+    Csum += mult * c;
+  }
+  Wsum = cta_tree_sum(Wsum, buf);
+  Csum = cta_tree_sum(Csum, buf);
+  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)q.weight * Wsum;
+  const float cE = (float)(Csum * E);
+  for (int p = t; p < N; p += blockDim.x) {
+    float gx = 0.f, gy = 0.f;
+    for (int tau = 1; tau <= K; ++tau) {
+      const float c = ct[tau];
+      if (c == 0.f) continue;
+      const float2 A = At[tau];
+      int j1 = p - tau, j2 = p + tau;
+      bool o1 = true, o2 = true;
+      if (q.periodic) {
+        j1 = j1 < 0 ? j1 + N : j1;
+        j2 = j2 >= N ? j2 - N : j2;
+      } else {
+        o1 = j1 >= 0;
+        o2 = j2 < N;
+      }
+      // (mult already in c: the -tau mirror contributes the same pair of terms)
+      if (o1) {
+        const float2 v = cmul(A, sg[j1]);
+        gx = fmaf(c, v.x, gx);
+        gy = fmaf(c, v.y, gy);
+      }
+      if (o2) {
+        const float2 v = cmul(cconj(A), sg[j2]);
+        gx = fmaf(c, v.x, gx);
+        gy = fmaf(c, v.y, gy);
+      }
+    }
+    const float2 sp = sg[p];
+    const float2 g = make_float2(q.weight * (gx - cE * sp.x), q.weight * (gy - cE * sp.y));
+    float2* gp = q.grad + (size_t)b * N + p;
+    *gp = q.accumulate ? cadd(*gp, g) : g;
+  }
+}
+
 #endif  // GRAF_API_UNIT
 
 }  // namespace graf

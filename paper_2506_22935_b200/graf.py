@@ -401,3 +401,19 @@ def xaf_backward(s1: torch.Tensor, s2: torch.Tensor, M: int, dA: torch.Tensor, *
                                       ctypes.c_void_p(s2.data_ptr()), ctypes.c_void_p(dA.data_ptr()), _ptr(g1),
                                       _ptr(g2), ctypes.c_void_p(wp), wn, _stream(stream)))
     return g1, g2
+
+
+def mainlobe_width(s: torch.Tensor, gamma: float, weight: float = 1.0, periodic: bool = False,
+                   loss: Optional[torch.Tensor] = None, grad: Optional[torch.Tensor] = None,
+                   accumulate: bool = False, stream=None):
+    """graf_mainlobe_width -> (weight*W [B] float64, weight*dW/ds* [B,N] complex64)."""
+    s = _check_s(s)
+    B, N = s.shape
+    if loss is None:
+        loss = torch.zeros((B,), dtype=torch.float64, device=s.device)
+    if grad is None:
+        grad = torch.zeros((B, N), dtype=torch.complex64, device=s.device)
+    L.check(L.lib().graf_mainlobe_width(B, N, ctypes.c_void_p(s.data_ptr()), float(gamma), float(weight),
+                                        int(bool(periodic)), _ptr(loss), ctypes.c_void_p(grad.data_ptr()),
+                                        int(bool(accumulate)), _stream(stream)))
+    return loss, grad

@@ -22,3 +22,5 @@ for c in ('c2match','c3match'):
     d=json.load(open('gpurun_out/bench_${TAG}_'+c+'.json')); r=d['roofline']; print(c, d['ms_per_step'], r['bound'], r['frac'])"
 timeout 600 python bench.py --config 2 --mode cross --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_c2cross.json 2> gpurun_out/bench_${TAG}_c2cross.err
 python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_c2cross.json')); r=d['roofline']; print('c2cross', d['ms_per_step'], r['bound'], r['frac'])"
+timeout 300 python bench.py --mode mlw --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_mlw.json 2> gpurun_out/bench_${TAG}_mlw.err
+python -c "import json; d=json.load(open('gpurun_out/bench_${TAG}_mlw.json')); print('mlw', d['ms_per_step'], d['value'])"

@@ -100,3 +100,19 @@ def test_match_argument_checks():
     spec.lambda_psl = 0.0
     with pytest.raises(graf.GrafError):
         graf.af_loss_grad(s, 32, spec, k_begin=-5, k_end=5)  # window misses delays of the region
+
+
+# ------------------------------------------------------------------ mainlobe width
+@pytest.mark.parametrize("N,periodic", [(1, False), (8, False), (37, False), (256, False), (64, True), (256, True),
+                                        (2048, False)])
+def test_mainlobe_width(N, periodic):
+    s = cg(2, N, N + 11)
+    for b_gamma in (0.5, 5.0):
+        E = np.array([O.energy(x) for x in s])
+        gam = float(b_gamma / E.mean() ** 2)
+        loss, g = graf.mainlobe_width(dev(s), gam, weight=0.7, periodic=periodic)
+        for b in range(2):
+            W, gref = O.mainlobe_width_and_grad(s[b], gam, periodic)
+            assert abs(loss[b].item() - 0.7 * W) <= 1e-4 * max(abs(0.7 * W), 1e-12) + 1e-9
+            sc = max(np.abs(gref).max(), 1e-30)
+            assert np.abs(g[b].cpu().numpy() - 0.7 * gref).max() <= 1e-4 * 0.7 * sc + 1e-12
