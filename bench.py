@@ -52,6 +52,13 @@ def workload(cid: int) -> dict:
     N, M, B = cfg["N"], cfg["M"], cfg["B"]
     rows = min(loss["k_max"], N - 1) + 1                       # folded delay rows k >= 0
     ffts = 2 if loss["lambda_psl"] == 0 else 3                  # fused ISL: fwd+inv; soft-PSL: fwd | fwd+inv
+    if ffts == 3 and not cfg["surface"]:
+        # band cache (graf_api.cu make_plan): a band of <= M/4 bins (cache <= 1 GiB) is kept
+        # from pass 1, so pass 2 runs only the inverse FFT -- count the FFTs actually executed
+        nband = 2 * min(loss["d_max"], M // 2) + 1
+        if nband <= M // 4 and B * rows * nband * 8 <= (1 << 30):
+            ffts = 2
+            note = "soft-PSL two-pass with the band cache: pass 2 reuses pass 1's in-band FFT outputs"
     flops = B * rows * ffts * 5.0 * M * math.log2(M)             # SURVEY.md §8(d) algorithmic FFT flops
     surf_bytes = 0
     if cfg["surface"]:

@@ -299,6 +299,21 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   off = align256(off + sizeof(graf_partials) * (size_t)B);
   pl.off_spad = off;
   if (!ci.s_smem) off = align256(off + sizeof(float2) * (size_t)B * (N + af->m));
+  // band cache: a two-pass loss (soft or hard PSL) on a narrow Doppler band keeps pass 1's
+  // in-band FFT outputs (nband complex per loss row) so pass 2 skips the lag product and
+  // the forward FFT; only when the band is at most M/4 bins and the cache at most 1 GiB
+  if (kind == Kind::LossGrad && L && (L->lambda_psl != 0.f || L->lambda_hpsl != 0.f) &&
+      af->out_kind == GRAF_OUT_NONE && !cross && pl.U > 0) {
+    const int dm = std::min(L->d_max, af->m / 2);
+    const int nband = 2 * dm + 1;
+    const size_t bytes = sizeof(float2) * (size_t)B * pl.U * nband;
+    if (nband <= af->m / 4 && bytes <= (size_t(1) << 30)) {
+      pl.cache_ok = true;
+      pl.nband = nband;
+      pl.off_cache = off;
+      off = align256(off + bytes);
+    }
+  }
   pl.total = off;
   return pl;
 }
@@ -651,15 +666,22 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     }
   } else {
     if (pl.U > 0) prof_mark(true, cs);
+    const bool use_cache = pl.cache_ok && !stats && dense && !match;
+    if (use_cache) {
+      rp.acache = reinterpret_cast<float2*>(static_cast<char*>(ws) + pl.off_cache);
+      rp.nband = pl.nband;
+    }
     if (!stats) {
       RowParams r1 = rp;
       r1.surface = nullptr;
+      r1.cache = use_cache ? 1 : 0;
       e = launch_rows(pl, r1, (int)af->batch, cs, K_FWD);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 1) launch");
       if ((st = run_partials_reduce(af, loss, pl, ws, comb, cs))) return st;
       stats = comb;
     }
     rp.stats = stats;
+    rp.cache = use_cache ? 2 : 0;
     if (pl.U > 0 && dense) {
       e = launch_rows(pl, rp, (int)af->batch, cs, match ? K_MATCH : K_PASS2);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (pass 2) launch");

@@ -68,6 +68,11 @@ struct RowParams {
   // (delay index from key_lo) * M + raw Doppler bin, ties -> lowest key (reading R23)
   int want_argmax;
   int key_lo;
+  // band cache of two-pass losses: pass 1 (K_FWD/K_FWDA, cache = 1) stores the FFT
+  // outputs of the loss band |d| <= d_max of every loss row, pass 2 (K_PASS2,
+  // cache = 2) reads them instead of recomputing the lag product and forward FFT
+  float2* acache;      // [B][U][nband]
+  int cache, nband;
   // cross-ambiguity (CROSS kernels): X = sum s[n] conj(s2[n-k]) W^{mn}; rows unfolded
   const float2* s2;    // [B][N]
   float2* gpart2;      // [B][P][N] partial dL/ds2*
@@ -628,6 +633,17 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       lrow = valid && p.loss_on &&
              (CROSS ? (k <= p.kloss && -k <= p.kloss) : (k <= p.kloss && (k % p.shard_count) == p.shard_index));
       const float mult = self ? 1.f : 2.f;
+      // pass 2 with the band cache: the row's in-band FFT outputs come from pass 1
+      const bool cread = (KIND == K_PASS2) && p.cache == 2;
+      float2* crow = p.acache + ((size_t)b * p.U + (valid ? u : 0)) * p.nband + p.d_max;
+      if (cread) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int m = t + e * T;
+          const int d = m < M / 2 ? m : m - M;
+          v[e] = (valid && ((band >> e) & 1)) ? crow[d] : make_float2(0.f, 0.f);
+        }
+      } else {
       if constexpr (!SPLIT) {
         const float2* a = sv + t;
         const float2* c = sv2 + t - k;
@@ -646,6 +662,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       stg_release();
       row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
       asm volatile("" ::: "memory");
+      if (FWD && p.cache == 1 && lrow) {
+        // pass 1: keep the loss band of this row for pass 2
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int m = t + e * T;
+          const int d = m < M / 2 ? m : m - M;
+          if ((band >> e) & 1) crow[d] = v[e];
+        }
+      }
+      }
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
       if (p.bulk) {

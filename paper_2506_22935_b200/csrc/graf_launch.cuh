@@ -40,6 +40,10 @@ struct Plan {
   bool fuse_req = false, fused = false;
   bool cross = false;   // cross-ambiguity (two waveforms, unfolded rows)
   size_t off_part = 0, off_gpart = 0, off_comb = 0, off_spad = 0, total = 0;
+  // band cache of two-pass losses (pass 1 stores the loss band, pass 2 reads it)
+  size_t off_cache = 0;
+  int nband = 0;
+  bool cache_ok = false;
 };
 
 
