@@ -59,6 +59,13 @@ def workload(cid: int) -> dict:
         if nband <= M // 4 and B * rows * nband * 8 <= (1 << 30):
             ffts = 2
             note = "soft-PSL two-pass with the band cache: pass 2 reuses pass 1's in-band FFT outputs"
+        full = (min(loss["k_max"], N - 1) == N - 1 and loss["d_max"] >= M // 2 and loss.get("ml_k", 0) == 0
+                and loss.get("ml_d", 0) == 0 and loss.get("normalize", 1) == 1)
+        if full:
+            # full-plane centred soft-PSL (R13): one pass of forward + inverse FFT per row,
+            # guarded fallback passes only for waveforms outside the validity rule
+            ffts = 2
+            note = "full-plane soft-PSL as one optimistic pass (R13), per-waveform guarded fallback"
     flops = B * rows * ffts * 5.0 * M * math.log2(M)             # SURVEY.md §8(d) algorithmic FFT flops
     surf_bytes = 0
     if cfg["surface"]:

@@ -5,6 +5,7 @@
 #define GRAF_API_UNIT 1   // this unit defines the non-template kernels of graf_kernels.cuh
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -263,7 +264,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   }
   const size_t nsig = cross ? 2 : 1;   // staged waveforms and gradient accumulator sets
   pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) +
-                              (cross ? (size_t)((N + std::max(af->m, 2 * N) + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
+                              (cross ? (size_t)((2 * N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? nsig * ci.S * N : 0) + (size_t)ci.tab1);
   if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512 && !af->periodic && !cross) {
     pl.gpad_ok = true;
@@ -296,7 +297,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
   pl.off_gpart = off;
   if (grad) off = align256(off + (cross ? 2 : 1) * sizeof(float2) * (size_t)B * pl.Pbound * N);
   pl.off_comb = off;
-  off = align256(off + sizeof(graf_partials) * (size_t)B);
+  off = align256(off + 2 * sizeof(graf_partials) * (size_t)B);   // combined partials (+ fallback set)
   pl.off_spad = off;
   if (!ci.s_smem) off = align256(off + sizeof(float2) * (size_t)B * (N + af->m));
   // band cache: a two-pass loss (soft or hard PSL) on a narrow Doppler band keeps pass 1's
@@ -443,7 +444,7 @@ graf_status check_ws(const Plan& pl, void* ws, size_t ws_bytes) {
 
 graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, const void* s,
                          void* ws, const graf_partials* global, double* loss, void* grad, bool norm_term,
-                         cudaStream_t st) {
+                         cudaStream_t st, const graf_partials* one = nullptr, const RowParams* rpo = nullptr) {
   FinalizeParams f;
   std::memset(&f, 0, sizeof(f));
   char* w = static_cast<char*>(ws);
@@ -461,6 +462,11 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
   f.T = (L && L->lambda_psl != 0.f) ? L->temperature : 1.f;
   f.invT = 1.f / f.T;
   f.lam_match = L ? L->lambda_match : 0.f;
+  f.one = one;
+  if (rpo) {
+    f.omega = rpo->omega;
+    f.xbar = rpo->xbar;
+  }
   f.loss = loss;
   f.grad = static_cast<float2*>(grad);
   if (pl.cross) {
@@ -476,6 +482,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
     fc.part = f.part + b0 * pl.P * kPart;
     fc.gpart = f.gpart + b0 * pl.P * (long long)af->n;
     fc.global = global ? global + b0 : nullptr;
+    fc.one = one ? one + b0 : nullptr;
     fc.loss = loss ? loss + b0 : nullptr;
     fc.grad = grad ? f.grad + b0 * af->n : nullptr;
     if (f.s2) {
@@ -493,7 +500,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
 }
 
 graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, void* ws,
-                                graf_partials* out, cudaStream_t st) {
+                                graf_partials* out, cudaStream_t st, int onepass = 0, float xbar = 0.f) {
   ReduceParams r;
   r.part = reinterpret_cast<const double*>(static_cast<char*>(ws) + pl.off_part);
   r.P = pl.P;
@@ -501,6 +508,8 @@ graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L,
   r.T = L->lambda_psl != 0.f ? L->temperature : 1.f;
   r.invT = 1.f / r.T;
   r.out = out;
+  r.onepass = onepass;
+  r.xbar = xbar;
   partials_reduce_kernel<<<(r.B + 3) / 4, 128, 0, st>>>(r);   // a warp per waveform
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++t_launches;
@@ -670,6 +679,32 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     if (use_cache) {
       rp.acache = reinterpret_cast<float2*>(static_cast<char*>(ws) + pl.off_cache);
       rp.nband = pl.nband;
+    }
+    // full-plane centred soft-PSL (reading R13): one optimistic pass with f' = lambda
+    // expm1((x - xbar)/T), then guarded fallback passes that only run the waveforms whose
+    // single pass is outside the R13 validity rule (max x - xbar > 40 T)
+    static const bool kOnePass = std::getenv("GRAF_NO_ONEPASS") == nullptr;
+    const bool onepass = kOnePass && !stats && rp.centred && !hpsl && !match && !use_cache &&
+                         rp.surface == nullptr && rp.shard_count <= 1 && pl.U > 0;
+    if (onepass) {
+      graf_partials* comb2 = comb + af->batch;
+      RowParams r0 = rp;
+      r0.onepass = 1;
+      e = launch_rows(pl, r0, (int)af->batch, cs, K_PASS2);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (single pass) launch");
+      if ((st = run_partials_reduce(af, loss, pl, ws, comb, cs, 1, rp.xbar))) return st;
+      RowParams r1 = rp;
+      r1.guard = comb;
+      e = launch_rows(pl, r1, (int)af->batch, cs, K_FWD);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (fallback pass 1) launch");
+      if ((st = run_partials_reduce(af, loss, pl, ws, comb2, cs))) return st;
+      RowParams r2 = rp;
+      r2.guard = comb;
+      r2.stats = comb2;
+      e = launch_rows(pl, r2, (int)af->batch, cs, K_PASS2);
+      if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (fallback pass 2) launch");
+      prof_mark(false, cs);
+      return run_finalize(af, loss, pl, s, ws, comb2, loss_out, grad, true, cs, comb, &rp);
     }
     if (!stats) {
       RowParams r1 = rp;

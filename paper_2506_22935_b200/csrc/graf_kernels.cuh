@@ -73,6 +73,13 @@ struct RowParams {
   // cache = 2) reads them instead of recomputing the lag product and forward FFT
   float2* acache;      // [B][U][nband]
   int cache, nband;
+  // optimistic single pass of the full-plane centred soft-PSL (K_PASS2, onepass = 1):
+  // f' = lambda expm1((x - xbar)/T) needs no global statistic (constant shifts of f'
+  // are gradient-neutral on a constant-sum region, reading R13) and 1/Z_c scales the
+  // result in the finalize.  The guarded fallback launches skip the waveforms whose
+  // single pass is valid (guard[b].reserved == 1).
+  int onepass;
+  const graf_partials* guard;
   // cross-ambiguity (CROSS kernels): X = sum s[n] conj(s2[n-k]) W^{mn}; rows unfolded
   const float2* s2;    // [B][N]
   float2* gpart2;      // [B][P][N] partial dL/ds2*
@@ -464,6 +471,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const int slot = threadIdx.x / T, t0 = threadIdx.x % T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float2* sg = p.s + (size_t)b * N;
+  if (p.guard && p.guard[b].reserved == 1.0) return;   // fallback launch: this waveform is done
 
   // ---- shared-memory carve-up: [scratch 64 doubles][s_pad N+M][exchange x S][g x S]
   // s_pad holds s[n] for n in [-N, M): N zeros, the N samples, M-N zeros, so the
@@ -471,10 +479,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   double* red = reinterpret_cast<double*>(smem);
   float2* s_pad = smem + 64;
   const int NP2 = (N + M + 1) & ~1;
-  // CROSS: the second waveform, zero-padded over [-N, max(M, 2N)): unfolded rows k < 0 read
-  // s2[n - k] up to n - k = 2N - 2 where s[n] != 0
+  // CROSS: the second waveform, zero-padded over [-N, M + N): unfolded rows k < 0 read
+  // s2[n - k] for every slot n < M (s[n] = 0 beyond N, but 0 * garbage may be NaN)
   float2* s2_pad = s_pad + (C::S_SMEM ? NP2 : 0);
-  const int NP2X = (N + (M > 2 * N ? M : 2 * N) + 1) & ~1;
+  const int NP2X = (2 * N + M + 1) & ~1;
   float2* xch = s2_pad + (CROSS ? NP2X : 0);
   float2* gacc_sh = xch + S * XS;
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
@@ -555,7 +563,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // pass-2 statistics from the combined partials (reading R13)
   float lse = 0.f, ebar = 0.f, invZc = 0.f;
   bool use_centred = false;
-  if constexpr (KIND == K_PASS2) {
+  if (KIND == K_PASS2 && p.onepass) {
+    use_centred = true;   // f' = lambda expm1((x - xbar)/T); 1/Z_c applied by the finalize
+    invZc = 1.f;
+  } else if constexpr (KIND == K_PASS2) {
     const graf_partials g = p.stats[b];
     // without a soft-PSL term the exp factor must vanish, not become 0 * inf
     lse = p.lam_psl != 0.f ? (float)(g.lse_max + (double)p.T * log(g.lse_sum)) : INFINITY;
@@ -772,7 +783,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       if (lrow) {
         const Mask inm = band & ~((k < 0 ? -k : k) <= p.ml_k ? mlb : (Mask)0);   // (CROSS rows may be k < 0)
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
-        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f;
+        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f, rowC1 = 0.f, rowM1 = -INFINITY;
         const float gsc = scaleG * mult;
         // match targets of rows +k and -k (K_MATCH; the host checked the window holds them)
         const float* tgp = nullptr;
@@ -825,7 +836,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             const float x = p.normalize ? chi * invE2 : chi;
             float fp;
             if (use_centred) {
-              fp = p.lam_psl * (expm1_fast((x - p.xbar) * p.invT) - ebar) * invZc;
+              const float ec = expm1_fast((x - p.xbar) * p.invT);
+              fp = p.lam_psl * (ec - ebar) * invZc;
+              rowC1 += in ? ec : 0.f;                      // (single pass: Z_c and the validity max)
+              rowM1 = fmaxf(rowM1, in ? x : -INFINITY);
             } else {
               fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
             }
@@ -838,6 +852,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         accS += (double)(mult * rowS);
         accF += (double)(mult * rowF);
         if constexpr (KIND == K_MATCH) accMt += (double)rowMt;
+        if constexpr (KIND == K_PASS2) {
+          if (p.onepass) {
+            accC += (double)(mult * rowC1);
+            accM = fmaxf(accM, rowM1);
+          }
+        }
         if constexpr (FWD) {
           if (want_lse && rowM > -INFINITY) {
             if (rowM > accM) {
@@ -982,6 +1002,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     const double F0 = block_sum<THREADS>(accF, scratch);
     double Z0 = 0.0, C0 = 0.0;
     float M0 = -INFINITY;
+    if constexpr (KIND == K_PASS2) {
+      if (p.onepass) {
+        M0 = block_max_all<THREADS>(accM, scratch);
+        C0 = block_sum<THREADS>(accC, scratch);
+      }
+    }
     if constexpr (FWD) {
       M0 = block_max_all<THREADS>(accM, scratch);
       if (want_lse) {
@@ -1098,6 +1124,8 @@ struct ReduceParams {
   int P, B;
   float invT, T;
   graf_partials* out;
+  int onepass;   // records of the single pass: reserved = 1 where it is valid (R13 rule)
+  float xbar;
 };
 
 // one warp per waveform: lane l merges records l, l+32, ... in order, then a fixed
@@ -1134,7 +1162,7 @@ __global__ void partials_reduce_kernel(ReduceParams r) {
     g.lse_sum = Z;
     g.cen_sum = Cs;
     g.psl_key = key;
-    g.reserved = 0.0;
+    g.reserved = (r.onepass && isfinite(Cs) && isfinite(m) && (m - (double)r.xbar) * (double)r.invT <= 40.0) ? 1.0 : 0.0;
     r.out[b] = g;
   }
 }
@@ -1158,6 +1186,10 @@ struct FinalizeParams {
   const float2* s2;
   const float2* gpart2;
   float2* grad2;
+  // single-pass soft-PSL results (valid where one[b].reserved == 1), else NULL
+  const graf_partials* one;
+  double omega;
+  float xbar;
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
@@ -1165,7 +1197,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   const int N = f.N;
   const float2* sg = f.s + (size_t)b * N;
   const float2* sg2 = f.s2 ? f.s2 + (size_t)b * N : nullptr;
-  __shared__ double sh[3];
+  __shared__ double sh[4];
+  const bool one = f.one && f.one[b].reserved == 1.0;   // single-pass soft-PSL result is valid
   if (threadIdx.x < 32) {
     const double e = warp_energy(sg, N, threadIdx.x);
     // cross-ambiguity: E1 E2 replaces E^2 (reading R25)
@@ -1183,7 +1216,15 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
         lse_merge(m, Z, rec[1], rec[2], f.T);
       }
       sh[1] = F;
-      if (f.loss) {
+      sh[3] = 1.0;
+      if (one) {
+        // single pass: p - pbar = (e - ebar) / Z_c; the gradient accumulated with f' = lambda e
+        // is scaled by 1/Z_c; LSE = xbar + T log Z_c (reading R13)
+        const double zc = f.omega + f.one[b].cen_sum;
+        sh[3] = 1.0 / zc;
+        if (f.loss)
+          f.loss[b] = f.lam_isl * (f.normalize ? S / (e * e2) : S) + f.lam_psl * ((double)f.xbar + (double)f.T * log(zc));
+      } else if (f.loss) {
         double Sg = S, mg = m, Zg = Z;
         if (f.global) {
           Sg = f.global[b].isl_sum;
@@ -1201,8 +1242,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   if (!f.grad) return;
   const double E = sh[0], E2 = sh[2];
   const bool nt = f.grad_norm_term && f.normalize;
+  const double gs = sh[3];   // 1/Z_c for the single pass, else 1
   // auto: -(2/E^3) F s;  cross: -F/(E1^2 E2) s1 and -F/(E1 E2^2) s2
-  const float coef = nt ? (float)((sg2 ? 1.0 : 2.0) * sh[1] / (E * E * E2)) : 0.f;
+  const float coef = nt ? (float)((sg2 ? 1.0 : 2.0) * sh[1] * gs / (E * E * E2)) : 0.f;
   const float coef2 = nt ? (float)(sh[1] / (E * E2 * E2)) : 0.f;
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
     double gx = 0, gy = 0;
@@ -1212,7 +1254,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
       gy += a.y;
     }
     const float2 sv = sg[n];
-    f.grad[(size_t)b * N + n] = make_float2((float)gx - coef * sv.x, (float)gy - coef * sv.y);
+    f.grad[(size_t)b * N + n] = make_float2((float)(gx * gs) - coef * sv.x, (float)(gy * gs) - coef * sv.y);
     if (sg2) {
       double hx = 0, hy = 0;
       for (int q = 0; q < f.P; ++q) {

@@ -155,6 +155,17 @@ def test_c5_shape_full_plane_softpsl_centred(N, M):
     check_loss_grad(s, M, spec)
 
 
+@pytest.mark.parametrize("N,M", [(256, 256), (1024, 1024)])
+def test_full_plane_softpsl_single_pass_and_fallback(N, M):
+    # the optimistic single pass (reading R13) and its per-waveform fallback: a random
+    # code is inside the validity rule, an LFM chirp's ridge (x ~ 1) is outside it; a
+    # mixed batch must match the oracle on both
+    from graf_inputs import lfm
+    s = np.stack([random_phase(SplitMix64(7_000_000), N), lfm(N, 1.0), random_phase(SplitMix64(7_000_001), N)])
+    spec = dict(CONFIGS[5]["loss"], k_max=N - 1, d_max=M // 2)
+    check_loss_grad(s.astype(np.complex64), M, spec)
+
+
 SPECS = [
     dict(k_max=5, d_max=4, ml_k=0, ml_d=0, lambda_isl=1.0, lambda_psl=0.0, normalize=1),
     dict(k_max=7, d_max=16, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05, normalize=1),
