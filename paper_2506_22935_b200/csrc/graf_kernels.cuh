@@ -738,8 +738,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
                 bulk_store(dst, src, rb);
               }
             };
-            if (wpos) put(out + ((size_t)b * surf_rows + rowp) * rb, sp);
-            if (wneg) put(out + ((size_t)b * surf_rows + rown) * rb, sp + rb);
+            if (wpos) put(out + ((size_t)b * surf_rows + (rowp < 0 ? 0 : rowp)) * rb, sp);
+            if (wneg) put(out + ((size_t)b * surf_rows + (rown < 0 ? 0 : rown)) * rb, sp + rb);
             bulk_commit();
           }
         }
@@ -748,8 +748,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         // column of frequency m in row +k: (m + lay) mod M; in row -k: (lay - m) mod M
         if (p.out_kind == GRAF_OUT_C64) {
           float2* out = reinterpret_cast<float2*>(p.surface);
-          float2* rp = out + ((size_t)b * surf_rows + rowp) * M;
-          float2* rn = out + ((size_t)b * surf_rows + rown) * M;
+          float2* rp = out + ((size_t)b * surf_rows + (rowp < 0 ? 0 : rowp)) * M;
+          float2* rn = out + ((size_t)b * surf_rows + (rown < 0 ? 0 : rown)) * M;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int m = t + e * T;
@@ -762,8 +762,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
         } else {
           float* out = reinterpret_cast<float*>(p.surface);
-          float* rp = out + ((size_t)b * surf_rows + rowp) * M;
-          float* rn = out + ((size_t)b * surf_rows + rown) * M;
+          float* rp = out + ((size_t)b * surf_rows + (rowp < 0 ? 0 : rowp)) * M;
+          float* rn = out + ((size_t)b * surf_rows + (rown < 0 ? 0 : rown)) * M;
           const bool absk = p.out_kind == GRAF_OUT_ABS_F32;
           const float sc = absk ? nrm : nrm * nrm;
 #pragma unroll
