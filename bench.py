@@ -130,12 +130,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def read_traffic(cid: int):
+def read_traffic(key: str):
+    """dram read+write bytes per launch of the dominant kernel from one ncu --set full
+    capture (profiles/traffic.json, key c<config>[fwd|per|match|cross]), else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     try:
-        return json.load(open(p)).get(f"c{cid}")
+        return json.load(open(p)).get(f"c{key}")
     except Exception:
         return None
 
@@ -503,7 +505,8 @@ def main():
         roof = {"bound": "alu", "achieved": fl_tf, "peak": round(FP32_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
                 "frac": fl_tf / FP32_PEAK_TFLOPS,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)"}
-    roof["traffic"] = read_traffic(w["cid"])
+    roof["traffic"] = read_traffic(f"{w['cid']}{'fwd' if args.mode == 'forward' else ''}"
+                                   f"{'per' if args.periodic else ''}{args.mode if args.mode in ('match', 'cross') else ''}")
     roof["kernel"] = (f"af_rows_kernel<{M}>" + (" (pass 1 + reduce + pass 2)" if w["loss"]["lambda_psl"] else "")
                       + (" with the fused cluster finalize" if launches_per_step == 1 and args.mode != "forward"
                          else ""))
