@@ -25,18 +25,11 @@ std::vector<TwUpload>& tw_uploaders() {
 namespace {
 
 thread_local std::string t_last_error;
-// cross-ambiguity context of the current graf_xaf_* call (NULL for the auto entry points)
-thread_local const void* t_s2 = nullptr;
-thread_local void* t_grad2 = nullptr;
-struct CrossScope {
-  CrossScope(const void* s2, void* g2) {
-    t_s2 = s2;
-    t_grad2 = g2;
-  }
-  ~CrossScope() {
-    t_s2 = nullptr;
-    t_grad2 = nullptr;
-  }
+// cross-ambiguity operands of a graf_xaf_* call (both NULL for the auto entry points)
+struct CallCtx {
+  const void* s2 = nullptr;
+  void* grad2 = nullptr;
+  bool cross() const { return s2 != nullptr; }
 };
 thread_local cudaEvent_t t_prof_start = nullptr, t_prof_stop = nullptr;
 
@@ -206,9 +199,8 @@ void folded_window(int kb, int ke, int* lo, int* hi) {
 
 enum class Kind { Forward, LossGrad, Backward };
 
-Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind) {
+Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool cross = false) {
   Plan pl;
-  const bool cross = (t_s2 != nullptr);
   pl.cross = cross;
   CfgInfo ci;
   cfg_for(af->m, &ci);
@@ -371,7 +363,7 @@ void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
   rp.xbar = (float)((M - 1) / rp.omega);
 }
 
-RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, void* ws) {
+RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, void* ws, const CallCtx& cx) {
   RowParams rp;
   std::memset(&rp, 0, sizeof(rp));
   rp.s = static_cast<const float2*>(s);
@@ -394,7 +386,7 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
   rp.part = reinterpret_cast<double*>(w + pl.off_part);
   rp.gpart = reinterpret_cast<float2*>(w + pl.off_gpart);
   if (pl.cross) {
-    rp.s2 = static_cast<const float2*>(t_s2);
+    rp.s2 = static_cast<const float2*>(cx.s2);
     rp.gpart2 = rp.gpart + (size_t)af->batch * pl.Pbound * af->n;
   }
   rp.s_pad = pl.s_smem ? nullptr : reinterpret_cast<const float2*>(w + pl.off_spad);
@@ -444,7 +436,8 @@ graf_status check_ws(const Plan& pl, void* ws, size_t ws_bytes) {
 
 graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, const void* s,
                          void* ws, const graf_partials* global, double* loss, void* grad, bool norm_term,
-                         cudaStream_t st, const graf_partials* one = nullptr, const RowParams* rpo = nullptr) {
+                         cudaStream_t st, const graf_partials* one = nullptr, const RowParams* rpo = nullptr,
+                         const CallCtx& cx = CallCtx{}) {
   FinalizeParams f;
   std::memset(&f, 0, sizeof(f));
   char* w = static_cast<char*>(ws);
@@ -470,9 +463,9 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
   f.loss = loss;
   f.grad = static_cast<float2*>(grad);
   if (pl.cross) {
-    f.s2 = static_cast<const float2*>(t_s2);
+    f.s2 = static_cast<const float2*>(cx.s2);
     f.gpart2 = f.gpart + (size_t)af->batch * pl.Pbound * af->n;
-    f.grad2 = static_cast<float2*>(t_grad2);
+    f.grad2 = static_cast<float2*>(cx.grad2);
   }
   const long long B = af->batch;
   for (long long b0 = 0; b0 < B; b0 += 65535) {
@@ -578,29 +571,29 @@ const char* graf_last_error(void) { return t_last_error.c_str(); }
 
 int32_t graf_last_launch_count(void) { return t_launches; }
 
-size_t graf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) {
+static size_t impl_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss, bool cross) {
   if (check_af(af) != GRAF_OK) return 0;
   if (loss && check_loss(af, loss) != GRAF_OK) return 0;
-  size_t need = make_plan(af, loss, Kind::LossGrad).total;
+  size_t need = make_plan(af, loss, Kind::LossGrad, cross).total;
   if (af->k_begin >= -(af->n - 1) && af->k_end <= af->n && af->k_begin < af->k_end)
-    need = std::max(need, make_plan(af, nullptr, Kind::Backward).total);
+    need = std::max(need, make_plan(af, nullptr, Kind::Backward, cross).total);
   return need;
 }
 
-graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s, void* surface,
+static graf_status impl_forward(const CallCtx& cx, const graf_af_desc* af, const graf_loss_desc* loss, const void* s, void* surface,
                             graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
   t_launches = 0;
   graf_status st = common_checks(af, loss, s, surface, false);
   if (st) return st;
   if (loss && !partials) return fail(GRAF_EINVAL, "loss given but partials is NULL");
-  Plan pl = make_plan(af, loss, Kind::Forward);
+  Plan pl = make_plan(af, loss, Kind::Forward, cx.cross());
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   if (reinterpret_cast<uintptr_t>(surface) & 15u) pl.bulk_ok = false;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   if (pl.U > 0 && (e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
-  RowParams rp = base_params(af, s, pl, ws);
+  RowParams rp = base_params(af, s, pl, ws, cx);
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
   if (loss) fill_loss(rp, af, loss);
   if (pl.U > 0) {
@@ -620,7 +613,7 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, 
   return GRAF_OK;
 }
 
-graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+static graf_status impl_loss_grad(const CallCtx& cx, const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
                               const graf_partials* global, double* loss_out, void* grad, void* surface, void* ws,
                               size_t ws_bytes, void* stream) {
   t_launches = 0;
@@ -629,7 +622,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
   if (!loss) return fail(GRAF_EINVAL, "loss descriptor is NULL");
   if (!grad) return fail(GRAF_EINVAL, "grad is NULL");
   if (!aligned8(grad)) return fail(GRAF_EINVAL, "grad is not 8-byte aligned");
-  Plan pl = make_plan(af, loss, Kind::LossGrad);
+  Plan pl = make_plan(af, loss, Kind::LossGrad, cx.cross());
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   if (reinterpret_cast<uintptr_t>(surface) & 15u) pl.bulk_ok = false;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -643,7 +636,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     // loss from global partials via the finalize path with P partial records absent
   }
   if (pl.U > 0 && (e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
-  RowParams rp = base_params(af, s, pl, ws);
+  RowParams rp = base_params(af, s, pl, ws, cx);
   fill_loss(rp, af, loss);
   rp.surface = af->out_kind != GRAF_OUT_NONE ? surface : nullptr;
   graf_partials* comb = reinterpret_cast<graf_partials*>(static_cast<char*>(ws) + pl.off_comb);
@@ -704,7 +697,7 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
       e = launch_rows(pl, r2, (int)af->batch, cs, K_PASS2);
       if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (fallback pass 2) launch");
       prof_mark(false, cs);
-      return run_finalize(af, loss, pl, s, ws, comb2, loss_out, grad, true, cs, comb, &rp);
+      return run_finalize(af, loss, pl, s, ws, comb2, loss_out, grad, true, cs, comb, &rp, cx);
     }
     if (!stats) {
       RowParams r1 = rp;
@@ -734,37 +727,56 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
     return GRAF_OK;
   }
   if (!pl.fused && dense) {
-    if ((st = run_finalize(af, loss, pl, s, ws, stats, loss_out, grad, true, cs))) return st;
+    if ((st = run_finalize(af, loss, pl, s, ws, stats, loss_out, grad, true, cs, nullptr, nullptr, cx))) return st;
   }
   if (hpsl) return run_psl(af, loss, pl, s, stats, loss_out, grad, dense ? 1 : 0, cs);
   return GRAF_OK;
 }
 
-graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
+static graf_status impl_backward(const CallCtx& cx, const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
                              size_t ws_bytes, void* stream) {
   t_launches = 0;
   graf_status st = common_checks(af, nullptr, s, nullptr, true);
   if (st) return st;
   if (!dA || !aligned8(dA)) return fail(GRAF_EINVAL, "dA is NULL or not 8-byte aligned");
   if (!grad || !aligned8(grad)) return fail(GRAF_EINVAL, "grad is NULL or not 8-byte aligned");
-  Plan pl = make_plan(af, nullptr, Kind::Backward);
+  Plan pl = make_plan(af, nullptr, Kind::Backward, cx.cross());
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   cudaError_t e = ensure_twiddles();
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   if ((e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
-  RowParams rp = base_params(af, s, pl, ws);
+  RowParams rp = base_params(af, s, pl, ws, cx);
   rp.dA = static_cast<const float2*>(dA);
   prof_mark(true, cs);
   e = launch_rows(pl, rp, (int)af->batch, cs, K_ADJ);
   if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (adjoint) launch");
   prof_mark(false, cs);
-  return run_finalize(af, nullptr, pl, s, ws, nullptr, nullptr, grad, false, cs);
+  return run_finalize(af, nullptr, pl, s, ws, nullptr, nullptr, grad, false, cs, nullptr, nullptr, cx);
+}
+
+size_t graf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) {
+  return impl_workspace_bytes(af, loss, false);
+}
+
+graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s, void* surface,
+                            graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
+  return impl_forward(CallCtx{}, af, loss, s, surface, partials, ws, ws_bytes, stream);
+}
+
+graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+                              const graf_partials* global, double* loss_out, void* grad, void* surface, void* ws,
+                              size_t ws_bytes, void* stream) {
+  return impl_loss_grad(CallCtx{}, af, loss, s, global, loss_out, grad, surface, ws, ws_bytes, stream);
+}
+
+graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
+                             size_t ws_bytes, void* stream) {
+  return impl_backward(CallCtx{}, af, s, dA, grad, ws, ws_bytes, stream);
 }
 
 size_t graf_xaf_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss) {
-  CrossScope cross(reinterpret_cast<const void*>(16), nullptr);   // any non-NULL: plan as cross
-  return graf_workspace_bytes(af, loss);
+  return impl_workspace_bytes(af, loss, true);
 }
 
 graf_status graf_xaf_forward(const graf_af_desc* af, const graf_loss_desc* loss, const void* s1, const void* s2,
@@ -773,8 +785,9 @@ graf_status graf_xaf_forward(const graf_af_desc* af, const graf_loss_desc* loss,
   if (!af) return fail(GRAF_EINVAL, "af descriptor is NULL");
   graf_status st = check_cross(af, loss, s2);
   if (st) return st;
-  CrossScope cross(s2, nullptr);
-  return graf_af_forward(af, loss, s1, surface, partials, ws, ws_bytes, stream);
+  CallCtx cx;
+  cx.s2 = s2;
+  return impl_forward(cx, af, loss, s1, surface, partials, ws, ws_bytes, stream);
 }
 
 graf_status graf_xaf_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss, const void* s1, const void* s2,
@@ -785,8 +798,10 @@ graf_status graf_xaf_loss_grad(const graf_af_desc* af, const graf_loss_desc* los
   graf_status st = check_cross(af, loss, s2);
   if (st) return st;
   if (!grad2 || !aligned8(grad2)) return fail(GRAF_EINVAL, "grad2 is NULL or not 8-byte aligned");
-  CrossScope cross(s2, grad2);
-  return graf_af_loss_grad(af, loss, s1, global, loss_out, grad1, surface, ws, ws_bytes, stream);
+  CallCtx cx;
+  cx.s2 = s2;
+  cx.grad2 = grad2;
+  return impl_loss_grad(cx, af, loss, s1, global, loss_out, grad1, surface, ws, ws_bytes, stream);
 }
 
 graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void* s2, const void* dA, void* grad1,
@@ -796,8 +811,10 @@ graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void
   graf_status st = check_cross(af, nullptr, s2);
   if (st) return st;
   if (!grad2 || !aligned8(grad2)) return fail(GRAF_EINVAL, "grad2 is NULL or not 8-byte aligned");
-  CrossScope cross(s2, grad2);
-  return graf_af_backward(af, s1, dA, grad1, ws, ws_bytes, stream);
+  CallCtx cx;
+  cx.s2 = s2;
+  cx.grad2 = grad2;
+  return impl_backward(cx, af, s1, dA, grad1, ws, ws_bytes, stream);
 }
 
 graf_status graf_set_profile_events(void* start, void* stop) {
