@@ -36,6 +36,50 @@ constexpr int kMaxM = 16384;
 // copy; ensure_twiddles() uploads all of them.
 static __device__ float2 g_tw[kMaxM];
 
+// Complex add / subtract.  sm_100 has paired fp32 instructions (FADD2 / FMUL2 /
+// FFMA2: one issue slot for the real and imaginary lanes); GRAF_F32X2 selects them
+// through PTX add/sub/mul/fma.rn.f32x2.  Same IEEE round-to-nearest results per lane.
+#if defined(GRAF_F32X2) && defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+__device__ __forceinline__ unsigned long long f2_pack(float2 a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(r);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(r);
+}
+// a * b = b.x (a.x, a.y) + b.y (-a.y, a.x): FMUL2 with a broadcast operand, then FFMA2
+// with the swapped, lane-negated pair (operand modifiers, no extra instructions)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  unsigned long long t, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2_pack(make_float2(b.x, b.x))), "l"(f2_pack(a)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(f2_pack(make_float2(-a.y, a.x))), "l"(f2_pack(make_float2(b.y, b.y))), "l"(t));
+  return f2_unpack(r);
+}
+// a * conj(b) = b.x (a.x, a.y) + b.y (a.y, -a.x)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  unsigned long long t, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2_pack(make_float2(b.x, b.x))), "l"(f2_pack(a)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(f2_pack(make_float2(a.y, -a.x))), "l"(f2_pack(make_float2(b.y, b.y))), "l"(t));
+  return f2_unpack(r);
+}
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
@@ -45,6 +89,7 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
+#endif
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
@@ -76,7 +121,11 @@ __device__ __forceinline__ float2 twc(float2 z) {
   } else {
     constexpr float c = cos32(J);
     constexpr float s = INV ? sin32(J) : -sin32(J);
+#if defined(GRAF_F32X2) && defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+    return cmul(z, make_float2(c, s));
+#else
     return make_float2(z.x * c - z.y * s, z.x * s + z.y * c);
+#endif
   }
 }
 
