@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -132,6 +133,12 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   }
   if (!pl.fixedP) {
     pl.P = choose_P(pl, B, occ, nsm);
+    // tuning knob (scripts/c2_rows.py): GRAF_FORCE_P=<P> overrides the model's choice
+    static const int kForceP = [] {
+      const char* v = std::getenv("GRAF_FORCE_P");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (kForceP > 0) pl.P = std::min(kForceP, std::max(pl.Pbound, 1));
     pl.fixedP = true;   // later passes of the same call reuse it
   }
   rp.fuse = 0;
