@@ -52,6 +52,7 @@ def workload(cid: int) -> dict:
     N, M, B = cfg["N"], cfg["M"], cfg["B"]
     rows = min(loss["k_max"], N - 1) + 1                       # folded delay rows k >= 0
     ffts = 2 if loss["lambda_psl"] == 0 else 3                  # fused ISL: fwd+inv; soft-PSL: fwd | fwd+inv
+    single = False
     if ffts == 3 and not cfg["surface"]:
         # band cache (graf_api.cu make_plan): a band of <= M/4 bins (cache <= 1 GiB) is kept
         # from pass 1, so pass 2 runs only the inverse FFT -- count the FFTs actually executed
@@ -65,6 +66,7 @@ def workload(cid: int) -> dict:
             # full-plane centred soft-PSL (R13): one pass of forward + inverse FFT per row,
             # guarded fallback passes only for waveforms outside the validity rule
             ffts = 2
+            single = True
             note = "full-plane soft-PSL as one optimistic pass (R13), per-waveform guarded fallback"
     flops = B * rows * ffts * 5.0 * M * math.log2(M)             # SURVEY.md §8(d) algorithmic FFT flops
     surf_bytes = 0
@@ -72,7 +74,7 @@ def workload(cid: int) -> dict:
         per = 8 if cfg["surface"] == "c64" else 4
         surf_bytes = B * (2 * N - 1) * M * per
     io_bytes = B * N * 8 * 2
-    return dict(cid=cid, cfg=cfg, loss=loss, N=N, M=M, B=B, rows=rows, ffts=ffts, flops=flops,
+    return dict(cid=cid, cfg=cfg, loss=loss, N=N, M=M, B=B, rows=rows, ffts=ffts, flops=flops, single=single,
                 surf_bytes=surf_bytes, io_bytes=io_bytes, note=note,
                 launches=(2 if loss["lambda_psl"] == 0 else 4))
 
@@ -507,7 +509,8 @@ def main():
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)"}
     roof["traffic"] = read_traffic(f"{w['cid']}{'fwd' if args.mode == 'forward' else ''}"
                                    f"{'per' if args.periodic else ''}{args.mode if args.mode in ('match', 'cross') else ''}")
-    roof["kernel"] = (f"af_rows_kernel<{M}>" + (" (pass 1 + reduce + pass 2)" if w["loss"]["lambda_psl"] else "")
+    two_pass = " (single pass + guarded fallback)" if w.get("single") else " (pass 1 + reduce + pass 2)"
+    roof["kernel"] = (f"af_rows_kernel<{M}>" + (two_pass if w["loss"]["lambda_psl"] else "")
                       + (" with the fused cluster finalize" if launches_per_step == 1 and args.mode != "forward"
                          else ""))
     roof["kernel_ms"] = kern_avg
