@@ -71,7 +71,7 @@ def main():
             if row[0]:
                 src = (cur, row[0])
                 text[src] = row[1].strip()
-            else:
+            elif src is not None:
                 try:
                     inst[src] += float(row[ie] or 0)
                     stall[src] += float(row[st] or 0)
