@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GRAF_ABI_VERSION 4
+#define GRAF_ABI_VERSION 5
 #define GRAF_MAX_M 16384
 
 typedef enum {
@@ -162,6 +162,34 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
  * ("IFFT operation (linear)", Eq. 15).  Linear in dA. */
 graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA,
                              void* grad, void* ws, size_t ws_bytes, void* stream);
+
+/* Delay-sharded SINGLE pass of the full-plane centred soft-PSL (DESIGN.md readings
+ * R13 and R27).  An unsharded graf_af_loss_grad already runs such a
+ * loss as one optimistic pass.  Across shards, the scale 1/Z_c and the validity rule
+ * need global sums, so the pass is split in two phases around the caller's exchange:
+ *   1. graf_af_loss_grad_sp_begin: this shard's rows (af->shard_index / shard_count >= 2)
+ *      run once with f' = lambda expm1((x - xbar)/T).  It writes this shard's partials
+ *      [B] (device), to be combined over ALL shards in rank order with
+ *      graf_combine_partials.  It keeps the unscaled gradient in `ws`.
+ *   2. graf_af_loss_grad_sp_end: takes `global` = the combined partials (device [B]).
+ *      It applies the R13 rule max x - xbar <= 40 T per waveform.  It writes loss[B]
+ *      (nullable) and this shard's grad[B][N], scaled by the global 1/Z_c.  The SUM over
+ *      shards is dL/ds*.  valid[B] (int32, nullable) is 1 where the rule holds.  Where it
+ *      fails, it writes loss NaN and grad 0; the caller then recomputes that batch with
+ *      the two-pass protocol (graf_af_forward partials -> combine -> graf_af_loss_grad
+ *      with `global`).  All shards see the same `global`, so they agree.
+ * Both phases take the same descriptors and the SAME workspace (graf_workspace_bytes),
+ * which must not be reused in between.
+ * Errors: GRAF_EINVAL for shard_count < 2, NULL or misaligned buffers, or a small
+ * workspace.  GRAF_EUNSUPPORTED unless graf_af_single_pass_eligible(af, loss) holds:
+ * the loss region is the full plane with no mainlobe cut, normalize = 1, no weights,
+ * lambda_psl != 0, no hard-PSL or match term, and no surface output. */
+int32_t graf_af_single_pass_eligible(const graf_af_desc* af, const graf_loss_desc* loss);
+graf_status graf_af_loss_grad_sp_begin(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+                                       graf_partials* partials, void* ws, size_t ws_bytes, void* stream);
+graf_status graf_af_loss_grad_sp_end(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+                                     const graf_partials* global, double* loss_out, void* grad,
+                                     int32_t* valid, void* ws, size_t ws_bytes, void* stream);
 
 /* Cross-ambiguity ("cross-ambiguity" for MIMO):
  *   X[k,m] = sum_n s1[n] conj(s2[n-k]) exp(-2 pi j m n / M),  k in [-(N-1), N-1],

@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # GRAF_LIB_PATH: tuning builds only (scripts/tune.py); the default is the in-tree library.
 LIB_PATH = os.environ.get("GRAF_LIB_PATH") or os.path.join(PKG, "libgraf.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_ENONFINITE, GRAF_EWORKSPACE = range(6)
 OUT_NONE, OUT_C64, OUT_ABS_F32, OUT_POW_F32 = range(4)
 DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
@@ -19,7 +19,8 @@ EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_wo
            "graf_af_forward", "graf_af_loss_grad", "graf_af_backward", "graf_combine_partials",
            "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
            "graf_phase_adam_step", "graf_xaf_workspace_bytes", "graf_xaf_forward", "graf_xaf_loss_grad",
-           "graf_xaf_backward", "graf_mainlobe_width")
+           "graf_xaf_backward", "graf_mainlobe_width", "graf_af_single_pass_eligible",
+           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end")
 
 
 class AfDesc(ctypes.Structure):
@@ -74,6 +75,14 @@ def lib() -> ctypes.CDLL:
         L.graf_af_backward.restype = c_int32
         L.graf_af_backward.argtypes = [POINTER(AfDesc), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                        c_void_p]
+        L.graf_af_single_pass_eligible.restype = c_int32
+        L.graf_af_single_pass_eligible.argtypes = [POINTER(AfDesc), POINTER(LossDesc)]
+        L.graf_af_loss_grad_sp_begin.restype = c_int32
+        L.graf_af_loss_grad_sp_begin.argtypes = [POINTER(AfDesc), POINTER(LossDesc), c_void_p, c_void_p, c_void_p,
+                                                 c_size_t, c_void_p]
+        L.graf_af_loss_grad_sp_end.restype = c_int32
+        L.graf_af_loss_grad_sp_end.argtypes = [POINTER(AfDesc), POINTER(LossDesc), c_void_p, c_void_p, c_void_p,
+                                               c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
         L.graf_combine_partials.restype = c_int32
         L.graf_combine_partials.argtypes = [POINTER(LossDesc), c_void_p, c_int32, c_int64, c_void_p, c_int32,
                                             c_void_p]

@@ -292,6 +292,12 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   off = align256(off + 2 * sizeof(graf_partials) * (size_t)B);   // combined partials (+ fallback set)
   pl.off_spad = off;
   if (!ci.s_smem) off = align256(off + sizeof(float2) * (size_t)B * (N + af->m));
+  if (kind == Kind::LossGrad && sc > 1 && !cross) {
+    pl.off_sp_rec = off;
+    off = align256(off + sizeof(double) * kPart * (size_t)B);
+    pl.off_sp_g = off;
+    off = align256(off + sizeof(float2) * (size_t)B * N);
+  }
   // band cache: a two-pass loss (soft or hard PSL) on a narrow Doppler band keeps pass 1's
   // in-band FFT outputs (nband complex per loss row) so pass 2 skips the lag product and
   // the forward FFT; only when the band is at most M/4 bins and the cache at most 1 GiB
@@ -437,7 +443,7 @@ graf_status check_ws(const Plan& pl, void* ws, size_t ws_bytes) {
 graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const Plan& pl, const void* s,
                          void* ws, const graf_partials* global, double* loss, void* grad, bool norm_term,
                          cudaStream_t st, const graf_partials* one = nullptr, const RowParams* rpo = nullptr,
-                         const CallCtx& cx = CallCtx{}) {
+                         const CallCtx& cx = CallCtx{}, int sp = 0) {
   FinalizeParams f;
   std::memset(&f, 0, sizeof(f));
   char* w = static_cast<char*>(ws);
@@ -456,6 +462,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
   f.invT = 1.f / f.T;
   f.lam_match = L ? L->lambda_match : 0.f;
   f.one = one;
+  f.sp = sp;
   if (rpo) {
     f.omega = rpo->omega;
     f.xbar = rpo->xbar;
@@ -733,6 +740,119 @@ static graf_status impl_loss_grad(const CallCtx& cx, const graf_af_desc* af, con
   return GRAF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Delay-sharded single pass of the full-plane centred soft-PSL (reading R13, R27).
+// Phase 1 runs this shard's rows once (f' = lambda expm1((x - xbar)/T)) and returns its
+// partials; the caller combines the shards' partials in rank order; phase 2 applies the
+// GLOBAL R13 rule and scales this shard's gradient by the global 1/Z_c.
+// ---------------------------------------------------------------------------
+static bool sp_eligible(const graf_af_desc* af, const graf_loss_desc* L) {
+  if (!af || !L || check_af(af) != GRAF_OK || check_loss(af, L) != GRAF_OK) return false;
+  if (af->out_kind != GRAF_OUT_NONE || L->lambda_hpsl != 0.f || L->lambda_match != 0.f) return false;
+  RowParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  fill_loss(rp, af, L);
+  return rp.centred != 0;
+}
+
+static graf_status sp_common(const graf_af_desc* af, const graf_loss_desc* L, const void* s, void* ws,
+                             size_t ws_bytes, Plan* pl) {
+  graf_status st = common_checks(af, L, s, nullptr, false);
+  if (st) return st;
+  if (!L) return fail(GRAF_EINVAL, "loss descriptor is NULL");
+  if ((af->shard_count <= 0 ? 1 : af->shard_count) < 2)
+    return fail(GRAF_EINVAL, "the sharded single pass needs shard_count >= 2 (unsharded calls use graf_af_loss_grad)");
+  if (!sp_eligible(af, L))
+    return fail(GRAF_EUNSUPPORTED, "sharded single pass: only the full-plane, normalised, unweighted soft-PSL "
+                                   "(graf_af_single_pass_eligible)");
+  *pl = make_plan(af, L, Kind::LossGrad, false);
+  return check_ws(*pl, ws, ws_bytes);
+}
+
+static graf_status impl_sp_begin(const graf_af_desc* af, const graf_loss_desc* L, const void* s,
+                                 graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
+  t_launches = 0;
+  Plan pl;
+  graf_status st = sp_common(af, L, s, ws, ws_bytes, &pl);
+  if (st) return st;
+  if (!partials || (reinterpret_cast<uintptr_t>(partials) & 7u)) return fail(GRAF_EINVAL, "partials is NULL or misaligned");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ensure_twiddles();
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  RowParams rp = base_params(af, s, pl, ws, CallCtx{});
+  fill_loss(rp, af, L);
+  Plan p0 = pl;
+  if (pl.U > 0) {
+    if ((e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
+    RowParams r0 = rp;
+    r0.onepass = 1;
+    prof_mark(true, cs);
+    e = launch_rows(pl, r0, (int)af->batch, cs, K_PASS2);
+    if (e != cudaSuccess) return cuda_fail(e, "af_rows_kernel (sharded single pass) launch");
+    prof_mark(false, cs);
+    p0 = pl;
+  } else {
+    p0.P = 0;   // this shard owns no rows: identity partials, zero gradient
+  }
+  if ((st = run_partials_reduce(af, L, p0, ws, partials, cs, 1, rp.xbar))) return st;
+  char* w = static_cast<char*>(ws);
+  SpFoldParams f;
+  f.part = reinterpret_cast<const double*>(w + pl.off_part);
+  f.gpart = reinterpret_cast<const float2*>(w + pl.off_gpart);
+  f.rec1 = reinterpret_cast<double*>(w + pl.off_sp_rec);
+  f.gsum = reinterpret_cast<float2*>(w + pl.off_sp_g);
+  f.P = p0.P;
+  f.N = af->n;
+  f.T = rp.T;
+  for (long long b0 = 0; b0 < af->batch; b0 += 65535) {
+    SpFoldParams fc = f;
+    const long long nb = std::min<long long>(65535, af->batch - b0);
+    fc.part = f.part + b0 * f.P * kPart;
+    fc.gpart = f.gpart + b0 * f.P * (long long)af->n;
+    fc.rec1 = f.rec1 + b0 * kPart;
+    fc.gsum = f.gsum + b0 * af->n;
+    sp_fold_kernel<<<(unsigned)nb, 256, 0, cs>>>(fc);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "sp_fold_kernel launch");
+    ++t_launches;
+  }
+  return GRAF_OK;
+}
+
+static graf_status impl_sp_end(const graf_af_desc* af, const graf_loss_desc* L, const void* s,
+                               const graf_partials* global, double* loss_out, void* grad, int32_t* valid, void* ws,
+                               size_t ws_bytes, void* stream) {
+  t_launches = 0;
+  Plan pl;
+  graf_status st = sp_common(af, L, s, ws, ws_bytes, &pl);
+  if (st) return st;
+  if (!global) return fail(GRAF_EINVAL, "global partials are NULL");
+  if (!grad || !aligned8(grad)) return fail(GRAF_EINVAL, "grad is NULL or not 8-byte aligned");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  RowParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  fill_loss(rp, af, L);
+  char* w = static_cast<char*>(ws);
+  graf_partials* comb = reinterpret_cast<graf_partials*>(w + pl.off_comb);
+  SpValidateParams v;
+  v.global = global;
+  v.out = comb;
+  v.valid = valid;
+  v.B = (int)af->batch;
+  v.xbar = rp.xbar;
+  v.invT = rp.invT;
+  sp_validate_kernel<<<(unsigned)((af->batch + 127) / 128), 128, 0, cs>>>(v);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sp_validate_kernel launch");
+  ++t_launches;
+  // the folded records / gradients of phase 1 play the role of P = 1 CTA partials
+  Plan p1 = pl;
+  p1.P = 1;
+  p1.Pbound = 1;
+  p1.off_part = pl.off_sp_rec;
+  p1.off_gpart = pl.off_sp_g;
+  return run_finalize(af, L, p1, s, ws, global, loss_out, grad, true, cs, comb, &rp, CallCtx{}, 1);
+}
+
 static graf_status impl_backward(const CallCtx& cx, const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,
                              size_t ws_bytes, void* stream) {
   t_launches = 0;
@@ -768,6 +888,21 @@ graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss
                               const graf_partials* global, double* loss_out, void* grad, void* surface, void* ws,
                               size_t ws_bytes, void* stream) {
   return impl_loss_grad(CallCtx{}, af, loss, s, global, loss_out, grad, surface, ws, ws_bytes, stream);
+}
+
+int32_t graf_af_single_pass_eligible(const graf_af_desc* af, const graf_loss_desc* loss) {
+  return sp_eligible(af, loss) ? 1 : 0;
+}
+
+graf_status graf_af_loss_grad_sp_begin(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+                                       graf_partials* partials, void* ws, size_t ws_bytes, void* stream) {
+  return impl_sp_begin(af, loss, s, partials, ws, ws_bytes, stream);
+}
+
+graf_status graf_af_loss_grad_sp_end(const graf_af_desc* af, const graf_loss_desc* loss, const void* s,
+                                     const graf_partials* global, double* loss_out, void* grad, int32_t* valid,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  return impl_sp_end(af, loss, s, global, loss_out, grad, valid, ws, ws_bytes, stream);
 }
 
 graf_status graf_af_backward(const graf_af_desc* af, const void* s, const void* dA, void* grad, void* ws,

@@ -1190,6 +1190,9 @@ struct FinalizeParams {
   const graf_partials* one;
   double omega;
   float xbar;
+  // delay-sharded single pass (graf_af_loss_grad_sp_end): the ISL sum comes from `global`,
+  // and a waveform whose global single pass is invalid gets loss NaN and grad 0
+  int sp;
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
@@ -1222,8 +1225,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
         // is scaled by 1/Z_c; LSE = xbar + T log Z_c (reading R13)
         const double zc = f.omega + f.one[b].cen_sum;
         sh[3] = 1.0 / zc;
+        const double Sg = f.sp ? f.global[b].isl_sum : S;
         if (f.loss)
-          f.loss[b] = f.lam_isl * (f.normalize ? S / (e * e2) : S) + f.lam_psl * ((double)f.xbar + (double)f.T * log(zc));
+          f.loss[b] = f.lam_isl * (f.normalize ? Sg / (e * e2) : Sg) + f.lam_psl * ((double)f.xbar + (double)f.T * log(zc));
+      } else if (f.sp) {
+        sh[3] = 0.0;   // invalid global single pass: the caller recomputes with two passes
+        if (f.loss) f.loss[b] = __longlong_as_double(0x7ff8000000000000ll);
       } else if (f.loss) {
         double Sg = S, mg = m, Zg = Z;
         if (f.global) {
@@ -1242,10 +1249,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   if (!f.grad) return;
   const double E = sh[0], E2 = sh[2];
   const bool nt = f.grad_norm_term && f.normalize;
-  const double gs = sh[3];   // 1/Z_c for the single pass, else 1
+  const double gs = sh[3];   // 1/Z_c for the single pass (0 for an invalid sharded one), else 1
   // auto: -(2/E^3) F s;  cross: -F/(E1^2 E2) s1 and -F/(E1 E2^2) s2
   const float coef = nt ? (float)((sg2 ? 1.0 : 2.0) * sh[1] * gs / (E * E * E2)) : 0.f;
   const float coef2 = nt ? (float)(sh[1] / (E * E2 * E2)) : 0.f;
+  if (f.sp && !one) {   // invalid sharded single pass: the unscaled sums may hold inf (expm1 overflow)
+    for (int n = threadIdx.x; n < N; n += blockDim.x) f.grad[(size_t)b * N + n] = make_float2(0.f, 0.f);
+    return;
+  }
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
     double gx = 0, gy = 0;
     for (int q = 0; q < f.P; ++q) {
@@ -1266,6 +1277,70 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
       f.grad2[(size_t)b * N + n] = make_float2((float)hx - coef2 * s2v.x, (float)hy - coef2 * s2v.y);
     }
   }
+}
+
+// Delay-sharded single pass, phase 1 tail: fold this shard's P CTA records and partial
+// gradients into one record and one unscaled gradient per waveform (fixed order), so
+// phase 2 needs neither the CTA count nor the per-CTA buffers.
+struct SpFoldParams {
+  const double* part;   // [B][P][kPart]
+  const float2* gpart;  // [B][P][N]
+  double* rec1;         // [B][kPart]
+  float2* gsum;         // [B][N]
+  int P, N;
+  float T;
+};
+
+__global__ void __launch_bounds__(256) sp_fold_kernel(SpFoldParams f) {
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    double S = 0, Z = 0, C = 0, F = 0, Mt = 0, m = -INFINITY;
+    for (int q = 0; q < f.P; ++q) {
+      const double* rec = f.part + ((size_t)b * f.P + q) * kPart;
+      S += rec[0];
+      lse_merge(m, Z, rec[1], rec[2], f.T);
+      C += rec[3];
+      F += rec[4];
+      Mt += rec[6];
+    }
+    double* o = f.rec1 + (size_t)b * kPart;
+    o[0] = S;
+    o[1] = m;
+    o[2] = Z;
+    o[3] = C;
+    o[4] = F;
+    o[5] = (double)0x7fffffff;
+    o[6] = Mt;
+    o[7] = 0.0;
+  }
+  for (int n = threadIdx.x; n < f.N; n += blockDim.x) {
+    double gx = 0, gy = 0;
+    for (int q = 0; q < f.P; ++q) {
+      const float2 a = f.gpart[((size_t)b * f.P + q) * f.N + n];
+      gx += a.x;
+      gy += a.y;
+    }
+    f.gsum[(size_t)b * f.N + n] = make_float2((float)gx, (float)gy);
+  }
+}
+
+// Phase 2 head: the R13 validity rule on the GLOBAL (rank-order combined) partials.
+struct SpValidateParams {
+  const graf_partials* global;
+  graf_partials* out;   // global with reserved = validity
+  int32_t* valid;       // may be NULL
+  int B;
+  float xbar, invT;
+};
+
+__global__ void sp_validate_kernel(SpValidateParams v) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= v.B) return;
+  graf_partials g = v.global[b];
+  const bool ok = isfinite(g.cen_sum) && isfinite(g.lse_max) && (g.lse_max - (double)v.xbar) * (double)v.invT <= 40.0;
+  g.reserved = ok ? 1.0 : 0.0;
+  v.out[b] = g;
+  if (v.valid) v.valid[b] = ok ? 1 : 0;
 }
 
 struct CombineParams {

@@ -45,6 +45,9 @@ struct Plan {
   size_t off_cache = 0;
   int nband = 0;
   bool cache_ok = false;
+  // delay-sharded single pass (graf_af_loss_grad_sp_begin / _end): one folded record and
+  // one unscaled gradient per waveform, kept in the workspace between the two phases
+  size_t off_sp_rec = 0, off_sp_g = 0;
 };
 
 

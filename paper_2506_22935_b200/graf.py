@@ -188,6 +188,49 @@ def af_backward(s: torch.Tensor, M: int, dA: torch.Tensor, *, k_begin=None, k_en
     return grad
 
 
+def single_pass_eligible(s: torch.Tensor, M: int, loss: LossSpec, shard=(0, 1), periodic: bool = False) -> bool:
+    """graf_af_single_pass_eligible: the full-plane centred soft-PSL that runs as one pass."""
+    d = _desc(s, M, None, "centered", None, None, False, shard, periodic)
+    return bool(L.lib().graf_af_single_pass_eligible(ctypes.byref(d), ctypes.byref(loss.desc())))
+
+
+def af_loss_grad_sp_begin(s: torch.Tensor, M: int, loss: LossSpec, shard, *, ws: Optional[Workspace] = None,
+                          stream=None, periodic: bool = False) -> torch.Tensor:
+    """graf_af_loss_grad_sp_begin: phase 1 of the delay-sharded single pass -> this
+    shard's partials [B, 6] (float64).  `ws` must be passed unchanged to phase 2."""
+    s = _check_s(s)
+    d = _desc(s, M, None, "centered", None, None, False, shard, periodic)
+    ld = loss.desc()
+    partials = torch.empty((s.shape[0], NPART), dtype=torch.float64, device=s.device)
+    wp, wn = (ws or _ws).get(workspace_bytes(d, ld), s.device)
+    L.check(L.lib().graf_af_loss_grad_sp_begin(ctypes.byref(d), ctypes.byref(ld), ctypes.c_void_p(s.data_ptr()),
+                                               ctypes.c_void_p(partials.data_ptr()), ctypes.c_void_p(wp), wn,
+                                               _stream(stream)))
+    return partials
+
+
+def af_loss_grad_sp_end(s: torch.Tensor, M: int, loss: LossSpec, shard, global_partials: torch.Tensor, *,
+                        ws: Optional[Workspace] = None, stream=None, periodic: bool = False):
+    """graf_af_loss_grad_sp_end: phase 2 -> (loss [B] float64, this shard's grad [B,N]
+    complex64, valid [B] int32).  Where valid is 0 the caller recomputes with two passes."""
+    s = _check_s(s)
+    d = _desc(s, M, None, "centered", None, None, False, shard, periodic)
+    ld = loss.desc()
+    B, N = s.shape
+    assert global_partials.dtype == torch.float64 and global_partials.shape == (B, NPART)
+    global_partials = global_partials.contiguous()
+    lo = torch.empty((B,), dtype=torch.float64, device=s.device)
+    g = torch.empty((B, N), dtype=torch.complex64, device=s.device)
+    valid = torch.empty((B,), dtype=torch.int32, device=s.device)
+    wp, wn = (ws or _ws).get(workspace_bytes(d, ld), s.device)
+    L.check(L.lib().graf_af_loss_grad_sp_end(ctypes.byref(d), ctypes.byref(ld), ctypes.c_void_p(s.data_ptr()),
+                                             ctypes.c_void_p(global_partials.data_ptr()),
+                                             ctypes.c_void_p(lo.data_ptr()), ctypes.c_void_p(g.data_ptr()),
+                                             ctypes.c_void_p(valid.data_ptr()), ctypes.c_void_p(wp), wn,
+                                             _stream(stream)))
+    return lo, g, valid
+
+
 def combine_partials(loss: LossSpec, shards: torch.Tensor, stream=None) -> torch.Tensor:
     """graf_combine_partials: shards [G,B,6] float64 -> [B,6], in shard order."""
     G, B, npart = shards.shape

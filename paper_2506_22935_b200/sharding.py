@@ -16,6 +16,13 @@ One process per GPU.  Two partitionings of the same hot path:
        its own partial sums), so the sum is the full dL/ds*.
   ISL-only losses are linear in the per-row sums, so step 1 is skipped and the
   per-shard losses are summed with the gradient.
+  The full-plane normalised soft-PSL (c5) runs ONE pass per shard instead of two
+  (reading R13 across shards, R27).  Phase 1 computes each shard's partials, including
+  the centred sum sum expm1((x - xbar)/T); those are all-gathered and combined.  Phase 2
+  scales each shard's gradient by the global 1/Z_c, and then comes the gradient
+  all_reduce.  If the global validity rule fails for any waveform, every rank falls back
+  to the two-pass protocol for the batch; all ranks hold the same combined partials, so
+  they all decide the same way.
 
 `backend` is the object that runs the per-shard compute; the default calls the
 C ABI (graf_af_forward / graf_af_loss_grad / graf_combine_partials).  Tests on CPU
@@ -46,6 +53,19 @@ class GrafBackend:
 
     def combine(self, spec, parts):
         return _graf.combine_partials(spec, parts)
+
+    def single_pass_eligible(self, s, M, spec, shard):
+        return _graf.single_pass_eligible(s, M, spec, shard)
+
+    _sp_ws = None   # the single pass keeps its unscaled gradient here between the phases
+
+    def sp_begin(self, s, M, spec, shard):
+        if GrafBackend._sp_ws is None:
+            GrafBackend._sp_ws = _graf.Workspace()
+        return _graf.af_loss_grad_sp_begin(s, M, spec, shard, ws=GrafBackend._sp_ws)
+
+    def sp_end(self, s, M, spec, glob, shard):
+        return _graf.af_loss_grad_sp_end(s, M, spec, shard, glob, ws=GrafBackend._sp_ws)
 
 
 def _world(group) -> Tuple[int, int]:
@@ -91,6 +111,16 @@ def delay_sharded_loss_grad(s: torch.Tensor, M: int, spec, group=None, backend=N
         dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
         return loss, g
+    if hasattr(backend, "sp_begin") and backend.single_pass_eligible(s, M, spec, shard):
+        # full-plane soft-PSL: one pass per shard, the global 1/Z_c applied in phase 2
+        part = backend.sp_begin(s, M, spec, shard)
+        gathered = [torch.empty_like(part) for _ in range(G)]
+        dist.all_gather(gathered, part.contiguous(), group=group)
+        glob = backend.combine(spec, torch.stack(gathered))
+        loss, g, valid = backend.sp_end(s, M, spec, glob, shard)
+        if bool(valid.all()):      # identical on every rank (same combined partials)
+            dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
+            return loss, g
     # soft-PSL: pass 1 partials -> all_gather -> combine (rank order) -> pass 2 -> all_reduce
     part = backend.forward_partials(s, M, spec, shard)
     gathered = [torch.empty_like(part) for _ in range(G)]

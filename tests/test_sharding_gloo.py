@@ -83,6 +83,108 @@ class OracleShardBackend:
         return torch.tensor(losses, dtype=torch.float64), torch.tensor(np.stack(grads))
 
 
+class OracleSinglePassBackend(OracleShardBackend):
+    """Adds the delay-sharded single pass (graf_af_loss_grad_sp_begin / _end, reading
+    R27) in float64: phase 1 returns (S, max x, 0, sum expm1((x - xbar)/T)) over the
+    shard's cells; phase 2 uses the global sums, f' = lambda_psl e / Z_c (ISL and
+    constant terms dropped, as on the GPU: their sum over all shards vanishes on the
+    full plane) and the R13 rule on the global max."""
+
+    def _full(self, spec):
+        return (spec.k_max >= self.N - 1 and spec.d_max >= self.M // 2 and spec.ml_k == 0 and spec.ml_d == 0
+                and spec.normalize == 1 and spec.lambda_psl != 0 and spec.w_k is None and spec.w_d is None)
+
+    def single_pass_eligible(self, s, M, spec, shard):
+        return self._full(spec)
+
+    def _xbar(self):
+        omega = (2 * self.N - 1) * self.M - 1
+        return omega, (self.M - 1) / omega
+
+    def sp_begin(self, s_b, M, spec, shard):
+        _, xbar = self._xbar()
+        out = []
+        for s in s_b.numpy():
+            rows, bins, mask, w, A = self._cells(s, spec, shard)
+            E = O.energy(s)
+            chi = np.abs(A) ** 2
+            x = chi / E ** 2
+            e = np.expm1((x[mask] - xbar) / spec.temperature)
+            c = float(np.max(x[mask])) if mask.any() else -np.inf
+            out.append([float(np.sum(w[mask] * chi[mask])), c, 0.0, float(np.sum(e)), 0.0, 0.0])
+        return torch.tensor(out, dtype=torch.float64)
+
+    def sp_end(self, s_b, M, spec, glob, shard):
+        omega, xbar = self._xbar()
+        T = spec.temperature
+        losses, grads, valid = [], [], []
+        for b, s in enumerate(s_b.numpy()):
+            rows, bins, mask, w, A = self._cells(s, spec, shard)
+            E = O.energy(s)
+            chi = np.abs(A) ** 2
+            x = chi / E ** 2
+            S, m, C = glob[b, 0].item(), glob[b, 1].item(), glob[b, 3].item()
+            ok = np.isfinite(C) and (m - xbar) / T <= 40.0
+            zc = omega + C
+            losses.append(spec.lambda_isl * S / E ** 2 + spec.lambda_psl * (xbar + T * np.log(zc)) if ok else np.nan)
+            fp = np.where(mask, spec.lambda_psl * np.expm1((x - xbar) / T) / zc, 0.0) if ok else np.zeros_like(x)
+            g = O.adjoint(s, self.M, fp * A / E ** 2, rows, bins) - (2.0 / E ** 3) * float(np.sum(fp * chi)) * s
+            grads.append(g)
+            valid.append(1 if ok else 0)
+        return (torch.tensor(losses, dtype=torch.float64), torch.tensor(np.stack(grads)),
+                torch.tensor(valid, dtype=torch.int32))
+
+
+def _sp_worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_22935_b200 import sharding, LossSpec
+        N, M, spec_d = case
+        s = np.stack([complex_gaussian(SplitMix64(700 + b), N) for b in range(3)]).astype(np.complex128)
+        be = OracleSinglePassBackend(N, M)
+        calls = []
+        fwd = be.forward_partials
+        be.forward_partials = lambda *a: (calls.append("two-pass"), fwd(*a))[1]
+        loss, g = sharding.delay_sharded_loss_grad(torch.tensor(s), M, LossSpec.from_dict(spec_d), backend=be)
+        q.put((rank, loss.numpy(), g.numpy(), calls))
+    finally:
+        dist.destroy_process_group()
+
+
+SP_CASES = [
+    # full plane, T = 0.05: the single pass is valid for every waveform
+    ((12, 16, dict(k_max=11, d_max=8, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05, normalize=1)), False),
+    # T = 0.004: max x - xbar > 40 T, every rank falls back to the two-pass protocol
+    ((12, 16, dict(k_max=11, d_max=8, lambda_isl=0.5, lambda_psl=1.0, temperature=0.004, normalize=1)), True),
+]
+
+
+@pytest.mark.parametrize("case,fallback", SP_CASES)
+def test_delay_sharded_single_pass_gloo_world2(case, fallback):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sp_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N, M, spec_d = case
+    s = np.stack([complex_gaussian(SplitMix64(700 + b), N) for b in range(3)]).astype(np.complex128)
+    ospec = O.LossSpec.from_dict(spec_d)
+    refs = [O.loss_and_grad(s[b], M, ospec) for b in range(3)]
+    L_ref = np.array([r[0] for r in refs])
+    g_ref = np.stack([r[1] for r in refs])
+    for rank, loss, g, calls in res:
+        assert (len(calls) > 0) == fallback, calls
+        np.testing.assert_allclose(loss, L_ref, rtol=1e-10)
+        np.testing.assert_allclose(g, g_ref, atol=1e-9 * np.abs(g_ref).max())
+
+
 def _free_port():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
