@@ -291,7 +291,9 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   pl.off_comb = off;
   off = align256(off + 2 * sizeof(graf_partials) * (size_t)B);   // combined partials (+ fallback set)
   pl.off_spad = off;
-  if (!ci.s_smem) off = align256(off + sizeof(float2) * (size_t)B * (N + af->m));
+  // pad_s_kernel rows (NL + M each, NL = N rounded up to even) + NL of tail slack: the
+  // adjoint's negative-delay rows read (and mask) up to N - 1 samples past a row's end
+  if (!ci.s_smem) off = align256(off + sizeof(float2) * ((size_t)B * (N + (N & 1) + af->m) + N + 1));
   if (kind == Kind::LossGrad && sc > 1 && !cross) {
     pl.off_sp_rec = off;
     off = align256(off + sizeof(double) * kPart * (size_t)B);

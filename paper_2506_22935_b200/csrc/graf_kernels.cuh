@@ -485,7 +485,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const int NP2X = (2 * N + M + 1) & ~1;
   float2* xch = s2_pad + (CROSS ? NP2X : 0);
   float2* gacc_sh = xch + S * XS;
-  const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (N + M) + N;
+  // global copy (M = 16384): rows of NL + M with NL = N rounded up to even, so every
+  // row and the sample origin are 16-byte aligned (the SPLIT path loads sample pairs)
+  const int NL = N + (N & 1);
+  const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (NL + M) + NL;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
   // per-slot accumulator stride: N, or 2N with N zero-padding on the left (p.gpad: folded
   // rows with M == N need no support predicates, out-of-support terms land in the pad)
@@ -661,12 +664,27 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
       } else {
+        // slots e and e + E2 hold the adjacent samples 2(t + eT) and 2(t + eT) + 1: one
+        // 16-byte load of the pair (s_pad rows are 16-byte aligned; the shifted factor
+        // only when k is even)
         const float2* a = sv + 2 * t;
         const float2* c = sv2 + 2 * t - k;
+        const float4* a4 = reinterpret_cast<const float4*>(a);
+        if ((k & 1) == 0) {
+          const float4* c4 = reinterpret_cast<const float4*>(c);
 #pragma unroll
-        for (int e = 0; e < E2; ++e) {
-          v[e] = cmulc(a[2 * e * T], c[2 * e * T]);
-          v[e + E2] = cmulc(a[2 * e * T + 1], c[2 * e * T + 1]);
+          for (int e = 0; e < E2; ++e) {
+            const float4 x = a4[e * T], y = c4[e * T];
+            v[e] = cmulc(make_float2(x.x, x.y), make_float2(y.x, y.y));
+            v[e + E2] = cmulc(make_float2(x.z, x.w), make_float2(y.z, y.w));
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E2; ++e) {
+            const float4 x = a4[e * T];
+            v[e] = cmulc(make_float2(x.x, x.y), c[2 * e * T]);
+            v[e + E2] = cmulc(make_float2(x.z, x.w), c[2 * e * T + 1]);
+          }
         }
       }
       // ---- a2: forward Doppler FFT
@@ -949,6 +967,69 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
             for (int e = 0; e < E; ++e) g2[toff(e)] = cadd(g2[toff(e)], cmulc(s2[toff(e)], v[e]));
           }
+        } else if constexpr (SPLIT && !CROSS) {
+          // SPLIT rows: process the slot pairs (j, j + E2) = samples (2(t + jT), 2(t + jT) + 1)
+          // together so the global s reads are 16-byte pair loads (term 2 always, term 1
+          // when k is even)
+          constexpr int CP = (E < kCorrChunk ? E : kCorrChunk) / 2;
+          const bool even = (k & 1) == 0;
+          {
+            const unsigned g1 = smem_u32(gacc + tb);
+            const float2* s1 = sv2 + tb - k;
+            static_for<0, E2 / CP>([&](auto c) {
+              constexpr int j0 = decltype(c)::value * CP;
+              float2 a[2 * CP], sl[2 * CP];
+              static_for<0, CP>([&](auto i) {
+                constexpr int j = j0 + decltype(i)::value;
+                a[2 * decltype(i)::value] = ld_shared_if<8 * toff(j)>(g1, (m1 >> j) & 1);
+                a[2 * decltype(i)::value + 1] = ld_shared_if<8 * toff(j + E2)>(g1, (m1 >> (j + E2)) & 1);
+              });
+              if (even) {
+                static_for<0, CP>([&](auto i) {
+                  constexpr int j = j0 + decltype(i)::value;
+                  const float4 q = reinterpret_cast<const float4*>(s1)[j * T];
+                  sl[2 * decltype(i)::value] = make_float2(q.x, q.y);
+                  sl[2 * decltype(i)::value + 1] = make_float2(q.z, q.w);
+                });
+              } else {
+                static_for<0, CP>([&](auto i) {
+                  constexpr int j = j0 + decltype(i)::value;
+                  sl[2 * decltype(i)::value] = s1[toff(j)];
+                  sl[2 * decltype(i)::value + 1] = s1[toff(j + E2)];
+                });
+              }
+              static_for<0, CP>([&](auto i) {
+                constexpr int j = j0 + decltype(i)::value;
+                constexpr int ii = 2 * decltype(i)::value;
+                st_shared_if<8 * toff(j)>(g1, cadd(a[ii], cmul(v[j], sl[ii])), (m1 >> j) & 1);
+                st_shared_if<8 * toff(j + E2)>(g1, cadd(a[ii + 1], cmul(v[j + E2], sl[ii + 1])), (m1 >> (j + E2)) & 1);
+              });
+            });
+          }
+          sync();
+          {
+            const unsigned g2 = smem_u32(gacc + tb - k);
+            const float4* s2 = reinterpret_cast<const float4*>(sv + tb);
+            static_for<0, E2 / CP>([&](auto c) {
+              constexpr int j0 = decltype(c)::value * CP;
+              float2 a[2 * CP];
+              float4 q[CP];
+              static_for<0, CP>([&](auto i) {
+                constexpr int j = j0 + decltype(i)::value;
+                a[2 * decltype(i)::value] = ld_shared_if<8 * toff(j)>(g2, (m1 >> j) & 1);
+                a[2 * decltype(i)::value + 1] = ld_shared_if<8 * toff(j + E2)>(g2, (m1 >> (j + E2)) & 1);
+                q[decltype(i)::value] = s2[j * T];
+              });
+              static_for<0, CP>([&](auto i) {
+                constexpr int j = j0 + decltype(i)::value;
+                constexpr int ii = 2 * decltype(i)::value;
+                const float4 x = q[decltype(i)::value];
+                st_shared_if<8 * toff(j)>(g2, cadd(a[ii], cmulc(make_float2(x.x, x.y), v[j])), (m1 >> j) & 1);
+                st_shared_if<8 * toff(j + E2)>(g2, cadd(a[ii + 1], cmulc(make_float2(x.z, x.w), v[j + E2])),
+                                               (m1 >> (j + E2)) & 1);
+              });
+            });
+          }
         } else {
           constexpr int CC = E < kCorrChunk ? E : kCorrChunk;
           {
@@ -1105,13 +1186,20 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #ifdef GRAF_API_UNIT   // the reductions and small kernels live in the ABI unit only
 // zero-padded copy of s for the global-memory path: s_pad[b][i] = s[b][i - N] for
 // i in [N, 2N), 0 elsewhere in [0, N + M)
+// rows of NL + M samples, NL = N rounded up to even: s[n] at NL + n, zeros elsewhere
+// (periodic: s[n + N] at NL + n for -N <= n < 0), so row starts and the origin are 16-byte aligned
 __global__ void pad_s_kernel(const float2* s, float2* s_pad, int N, int M, long long B, int periodic) {
-  const long long total = B * (long long)(N + M);
+  const int NL = N + (N & 1);
+  const long long R = NL + M;
+  const long long total = B * R;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const long long b = i / (N + M);
-    const int j = (int)(i - b * (N + M));
-    s_pad[i] = (j < 2 * N && (j >= N || periodic)) ? s[b * N + (j >= N ? j - N : j)] : make_float2(0.f, 0.f);
+    const long long b = i / R;
+    const int n = (int)(i - b * R) - NL;
+    float2 v = make_float2(0.f, 0.f);
+    if (n >= 0 && n < N) v = s[b * N + n];
+    else if (periodic && n < 0 && n >= -N) v = s[b * N + n + N];
+    s_pad[i] = v;
   }
 }
 
