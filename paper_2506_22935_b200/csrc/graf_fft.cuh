@@ -334,6 +334,12 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
   constexpr int NS = pass_ns(M, E, P);
   constexpr int Q = E / R;
   constexpr bool LAST = (NS * R == M);
+  // last pass with several butterflies per thread (a remainder radix R < E): t + qT < NS,
+  // so its bases W_M^{t + qT} = W_M^t W_E^q need ONE table read per pass (the W_E^q
+  // factors are compile-time constants after unrolling)
+  constexpr bool LAST_BASE = LAST && Q > 1 && NS > 1 && E <= 32 && (32 % E) == 0 && !Twiddles<M, E>::CACHE;
+  float2 lb0 = make_float2(1.f, 0.f);
+  if constexpr (LAST_BASE) lb0 = __ldg(&g_tw[t * (kMaxM / M)]);
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     float2 x[R];
@@ -359,9 +365,14 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
 #ifdef GRAF_HOLD_BASES
         tw_powers<R>(tw.base[tw_offset(M, E, P) + q], w);
 #else
-        // base twiddle re-read per use from the L1-resident table (frees registers)
-        const int jm = (t + q * T) & (NS - 1);
-        tw_powers<R>(__ldg(&g_tw[(jm * (M / (NS * R))) * (kMaxM / M)]), w);
+        if constexpr (LAST_BASE) {
+          const int J = (q * (32 / E)) % 32;
+          tw_powers<R>(q == 0 ? lb0 : cmul(lb0, make_float2(cos32(J), -sin32(J))), w);
+        } else {
+          // base twiddle re-read per use from the L1-resident table (frees registers)
+          const int jm = (t + q * T) & (NS - 1);
+          tw_powers<R>(__ldg(&g_tw[(jm * (M / (NS * R))) * (kMaxM / M)]), w);
+        }
 #endif
 #pragma unroll
         for (int r = 1; r < R; ++r) x[r] = INV ? cmulc(x[r], w[r]) : cmul(x[r], w[r]);
