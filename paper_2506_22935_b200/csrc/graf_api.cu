@@ -199,6 +199,12 @@ void folded_window(int kb, int ke, int* lo, int* hi) {
 
 enum class Kind { Forward, LossGrad, Backward };
 
+// elements of one global s copy (pad_s_kernel): B rows of NL + M, NL = N rounded up to
+// even, plus N + 2 of tail slack (kept even so the second copy starts 16-byte aligned)
+size_t spad_elems(long long B, int N, int M) {
+  return (size_t)B * (size_t)(N + (N & 1) + M) + (size_t)(N + (N & 1) + 2);
+}
+
 Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool cross = false) {
   Plan pl;
   pl.cross = cross;
@@ -291,9 +297,10 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   pl.off_comb = off;
   off = align256(off + 2 * sizeof(graf_partials) * (size_t)B);   // combined partials (+ fallback set)
   pl.off_spad = off;
-  // pad_s_kernel rows (NL + M each, NL = N rounded up to even) + NL of tail slack: the
-  // adjoint's negative-delay rows read (and mask) up to N - 1 samples past a row's end
-  if (!ci.s_smem) off = align256(off + sizeof(float2) * ((size_t)B * (N + (N & 1) + af->m) + N + 1));
+  // pad_s_kernel rows (NL + M each, NL = N rounded up to even), twice (the second copy
+  // shifted by one sample), each + tail slack: the adjoint's negative-delay rows read (and
+  // mask) up to N samples past a row's end
+  if (!ci.s_smem) off = align256(off + 2 * sizeof(float2) * spad_elems(B, N, af->m));
   if (kind == Kind::LossGrad && sc > 1 && !cross) {
     pl.off_sp_rec = off;
     off = align256(off + sizeof(double) * kPart * (size_t)B);
@@ -398,6 +405,7 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
     rp.gpart2 = rp.gpart + (size_t)af->batch * pl.Pbound * af->n;
   }
   rp.s_pad = pl.s_smem ? nullptr : reinterpret_cast<const float2*>(w + pl.off_spad);
+  rp.s_pad1 = pl.s_smem ? nullptr : rp.s_pad + spad_elems(af->batch, af->n, af->m);
   return rp;
 }
 
@@ -405,9 +413,11 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
 cudaError_t prepare_spad(const Plan& pl, const graf_af_desc* af, const void* s, void* ws, cudaStream_t st) {
   if (pl.s_smem) return cudaSuccess;
   float2* sp = reinterpret_cast<float2*>(static_cast<char*>(ws) + pl.off_spad);
+  float2* sp1 = sp + spad_elems(af->batch, af->n, af->m);
   const long long total = af->batch * (long long)(af->n + af->m);
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-  pad_s_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(s), sp, af->n, af->m, af->batch, af->periodic);
+  pad_s_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(s), sp, sp1, af->n, af->m, af->batch,
+                                       af->periodic);
   const cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++t_launches;
   return e;

@@ -58,7 +58,8 @@ struct RowParams {
   // outputs
   double* part;        // [B][P][kPart]
   float2* gpart;       // [B][P][N]
-  const float2* s_pad; // [B][N+M] zero-padded s (global-memory path, M > 8192)
+  const float2* s_pad; // [B][NL+M] zero-padded s (global-memory path, M > 8192)
+  const float2* s_pad1; // the same rows shifted by one sample (odd delays read aligned pairs)
   int bulk;            // surface rows staged in shared memory + bulk async copies: 1 dedicated
                        // buffer (stg_floats per slot), 2 aliased to the slot's exchange buffer
   int stg_floats;      // staging floats per row slot (2*M*{1,2}: rows +k and -k)
@@ -489,6 +490,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // row and the sample origin are 16-byte aligned (the SPLIT path loads sample pairs)
   const int NL = N + (N & 1);
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (NL + M) + NL;
+  // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
+  const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * (NL + M) + NL + 1;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
   // per-slot accumulator stride: N, or 2N with N zero-padding on the left (p.gpad: folded
   // rows with M == N need no support predicates, out-of-support terms land in the pad)
@@ -679,11 +682,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             v[e + E2] = cmulc(make_float2(x.z, x.w), make_float2(y.z, y.w));
           }
         } else {
+          // odd k: the shifted copy holds s[2t - k + 2eT] at an even (aligned) position
+          const float4* c4 = reinterpret_cast<const float4*>(sv_o + 2 * t - k);
 #pragma unroll
           for (int e = 0; e < E2; ++e) {
-            const float4 x = a4[e * T];
-            v[e] = cmulc(make_float2(x.x, x.y), c[2 * e * T]);
-            v[e + E2] = cmulc(make_float2(x.z, x.w), c[2 * e * T + 1]);
+            const float4 x = a4[e * T], y = c4[e * T];
+            v[e] = cmulc(make_float2(x.x, x.y), make_float2(y.x, y.y));
+            v[e + E2] = cmulc(make_float2(x.z, x.w), make_float2(y.z, y.w));
           }
         }
       }
@@ -984,20 +989,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
                 a[2 * decltype(i)::value] = ld_shared_if<8 * toff(j)>(g1, (m1 >> j) & 1);
                 a[2 * decltype(i)::value + 1] = ld_shared_if<8 * toff(j + E2)>(g1, (m1 >> (j + E2)) & 1);
               });
-              if (even) {
-                static_for<0, CP>([&](auto i) {
-                  constexpr int j = j0 + decltype(i)::value;
-                  const float4 q = reinterpret_cast<const float4*>(s1)[j * T];
-                  sl[2 * decltype(i)::value] = make_float2(q.x, q.y);
-                  sl[2 * decltype(i)::value + 1] = make_float2(q.z, q.w);
-                });
-              } else {
-                static_for<0, CP>([&](auto i) {
-                  constexpr int j = j0 + decltype(i)::value;
-                  sl[2 * decltype(i)::value] = s1[toff(j)];
-                  sl[2 * decltype(i)::value + 1] = s1[toff(j + E2)];
-                });
-              }
+              // (odd k: from the shifted copy, where the pair is aligned too)
+              const float4* s14 = reinterpret_cast<const float4*>(even ? s1 : sv_o + tb - k);
+              static_for<0, CP>([&](auto i) {
+                constexpr int j = j0 + decltype(i)::value;
+                const float4 q = s14[j * T];
+                sl[2 * decltype(i)::value] = make_float2(q.x, q.y);
+                sl[2 * decltype(i)::value + 1] = make_float2(q.z, q.w);
+              });
               static_for<0, CP>([&](auto i) {
                 constexpr int j = j0 + decltype(i)::value;
                 constexpr int ii = 2 * decltype(i)::value;
@@ -1187,19 +1186,25 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 // zero-padded copy of s for the global-memory path: s_pad[b][i] = s[b][i - N] for
 // i in [N, 2N), 0 elsewhere in [0, N + M)
 // rows of NL + M samples, NL = N rounded up to even: s[n] at NL + n, zeros elsewhere
-// (periodic: s[n + N] at NL + n for -N <= n < 0), so row starts and the origin are 16-byte aligned
-__global__ void pad_s_kernel(const float2* s, float2* s_pad, int N, int M, long long B, int periodic) {
+// (periodic: s[n + N] at NL + n for -N <= n < 0), so row starts and the origin are 16-byte
+// aligned.  s_pad1 holds the same rows shifted by one sample (s[n] at NL + 1 + n), so a
+// pair starting at an odd sample index is aligned there.
+__global__ void pad_s_kernel(const float2* s, float2* s_pad, float2* s_pad1, int N, int M, long long B,
+                             int periodic) {
   const int NL = N + (N & 1);
   const long long R = NL + M;
   const long long total = B * R;
+  auto val = [&](long long b, int n) {
+    if (n >= 0 && n < N) return s[b * N + n];
+    if (periodic && n < 0 && n >= -N) return s[b * N + n + N];
+    return make_float2(0.f, 0.f);
+  };
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long b = i / R;
-    const int n = (int)(i - b * R) - NL;
-    float2 v = make_float2(0.f, 0.f);
-    if (n >= 0 && n < N) v = s[b * N + n];
-    else if (periodic && n < 0 && n >= -N) v = s[b * N + n + N];
-    s_pad[i] = v;
+    const int j = (int)(i - b * R);
+    s_pad[i] = val(b, j - NL);
+    s_pad1[i] = val(b, j - NL - 1);
   }
 }
 
