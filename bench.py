@@ -687,6 +687,16 @@ class TimedBackend:
     def combine(self, *a):
         return self.inner.combine(*a)
 
+    # delay-sharded single pass (full-plane soft-PSL, c5): phase 1 holds the row kernels
+    def single_pass_eligible(self, *a):
+        return self.inner.single_pass_eligible(*a)
+
+    def sp_begin(self, *a):
+        return self._timed(0, self.inner.sp_begin, *a)
+
+    def sp_end(self, *a):
+        return self.inner.sp_end(*a)
+
     def kernel_ms(self):
         return self.ev[0].elapsed_time(self.ev[1]) + self.ev[2].elapsed_time(self.ev[3])
 
