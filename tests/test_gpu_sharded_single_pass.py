@@ -112,3 +112,25 @@ def test_sharded_single_pass_argument_errors():
         graf.af_loss_grad_sp_begin(ds, M, masked, (0, 2))
     isl_only = graf.LossSpec(k_max=N - 1, d_max=M // 2, lambda_isl=1.0)
     assert not graf.single_pass_eligible(ds, M, isl_only, (0, 2))
+
+
+@pytest.mark.parametrize("N,G", [(64, 2), (256, 3)])
+def test_sharded_single_pass_periodic(N, G):
+    # the paper's circular surface (periodic = 1, M = N): the folded residues k % G == r
+    s = np.stack([random_phase(SplitMix64(8_300_000 + b), N) for b in range(2)])
+    spec_d = dict(CONFIGS[5]["loss"], k_max=N, d_max=N)
+    spec = graf.LossSpec.from_dict(spec_d)
+    ds = dev(s)
+    assert graf.single_pass_eligible(ds, N, spec, (0, G), periodic=True)
+    ws = [graf.graf.Workspace() for _ in range(G)]
+    parts = torch.stack([graf.af_loss_grad_sp_begin(ds, N, spec, (r, G), ws=ws[r], periodic=True) for r in range(G)])
+    glob = graf.combine_partials(spec, parts)
+    outs = [graf.af_loss_grad_sp_end(ds, N, spec, (r, G), glob, ws=ws[r], periodic=True) for r in range(G)]
+    assert outs[0][2].cpu().numpy().tolist() == [1, 1]
+    g = sum(o[1] for o in outs).cpu().numpy()
+    ospec = O.LossSpec.from_dict(spec_d)
+    for b in range(2):
+        L_ref, g_ref, t = O.loss_and_grad(s[b], N, ospec, periodic=True)
+        assert abs(outs[G - 1][0][b].item() - L_ref) <= 1e-4 * abs(L_ref)
+        tol = 1e-4 * max(np.abs(g_ref).max(), t["sigma_g"])
+        assert np.abs(g[b] - g_ref).max() <= tol
