@@ -490,6 +490,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // row and the sample origin are 16-byte aligned (the SPLIT path loads sample pairs)
   const int NL = N + (N & 1);
   const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (NL + M) + NL;
+  // zero-padded Doppler axis (2N <= M, aperiodic): time slots e >= E/2 hold n >= M/2 >= N
+  // (compiled for M >= 2048 only: the extra code path measured 3 % slower at M = 1024)
+  constexpr bool kHalfSizes = (M >= 2048) && !SPLIT;
+  const bool half = kHalfSizes && !p.periodic && 2 * N <= M;
   // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
   const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * (NL + M) + NL + 1;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
@@ -664,8 +668,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       if constexpr (!SPLIT) {
         const float2* a = sv + t;
         const float2* c = sv2 + t - k;
+        if (kHalfSizes && half) {
+          // zero-padded row (2N <= M): the samples n = t + eT >= M/2 >= N are zero
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
+          for (int e = 0; e < E / 2; ++e) v[e] = cmulc(a[e * T], c[e * T]);
+#pragma unroll
+          for (int e = E / 2; e < E; ++e) v[e] = make_float2(0.f, 0.f);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
+        }
       } else {
         // slots e and e + E2 hold the adjacent samples 2(t + eT) and 2(t + eT) + 1: one
         // 16-byte load of the pair (s_pad rows are 16-byte aligned; the shifted factor
@@ -1031,40 +1043,51 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
         } else {
           constexpr int CC = E < kCorrChunk ? E : kCorrChunk;
-          {
-            // CROSS: term 1 is dL/ds* with the conjugated factor s2[n-k]
-            const unsigned g1 = smem_u32(gacc + tb);
-            const float2* s1 = sv2 + tb - k;
-            static_for<0, E / CC>([&](auto c) {
-              constexpr int e0 = decltype(c)::value * CC;
-              float2 a[CC];
-              static_for<0, CC>([&](auto i) {
-                constexpr int e = e0 + decltype(i)::value;
-                a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g1, (m1 >> e) & 1);
+          // NCH chunks of CC slots; a zero-padded row (2N <= M) has no support in the upper
+          // half of the slots (n >= M/2 >= N), so it runs the lower half only
+          auto corr = [&](auto nch) {
+            constexpr int NCH = decltype(nch)::value;
+            {
+              // CROSS: term 1 is dL/ds* with the conjugated factor s2[n-k]
+              const unsigned g1 = smem_u32(gacc + tb);
+              const float2* s1 = sv2 + tb - k;
+              static_for<0, NCH>([&](auto c) {
+                constexpr int e0 = decltype(c)::value * CC;
+                float2 a[CC];
+                static_for<0, CC>([&](auto i) {
+                  constexpr int e = e0 + decltype(i)::value;
+                  a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g1, (m1 >> e) & 1);
+                });
+                static_for<0, CC>([&](auto i) {
+                  constexpr int e = e0 + decltype(i)::value;
+                  st_shared_if<8 * toff(e)>(g1, cadd(a[decltype(i)::value], cmul(v[e], s1[toff(e)])), (m1 >> e) & 1);
+                });
               });
-              static_for<0, CC>([&](auto i) {
-                constexpr int e = e0 + decltype(i)::value;
-                st_shared_if<8 * toff(e)>(g1, cadd(a[decltype(i)::value], cmul(v[e], s1[toff(e)])), (m1 >> e) & 1);
+            }
+            sync();
+            {
+              // CROSS: term 2 is dL/ds2* (its own accumulator) with s[n]
+              const unsigned g2 = smem_u32((CROSS ? gacc2 : gacc) + tb - k);
+              const float2* s2 = sv + tb;
+              static_for<0, NCH>([&](auto c) {
+                constexpr int e0 = decltype(c)::value * CC;
+                float2 a[CC];
+                static_for<0, CC>([&](auto i) {
+                  constexpr int e = e0 + decltype(i)::value;
+                  a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g2, (m1 >> e) & 1);
+                });
+                static_for<0, CC>([&](auto i) {
+                  constexpr int e = e0 + decltype(i)::value;
+                  st_shared_if<8 * toff(e)>(g2, cadd(a[decltype(i)::value], cmulc(s2[toff(e)], v[e])), (m1 >> e) & 1);
+                });
               });
-            });
-          }
-          sync();
-          {
-            // CROSS: term 2 is dL/ds2* (its own accumulator) with s[n]
-            const unsigned g2 = smem_u32((CROSS ? gacc2 : gacc) + tb - k);
-            const float2* s2 = sv + tb;
-            static_for<0, E / CC>([&](auto c) {
-              constexpr int e0 = decltype(c)::value * CC;
-              float2 a[CC];
-              static_for<0, CC>([&](auto i) {
-                constexpr int e = e0 + decltype(i)::value;
-                a[decltype(i)::value] = ld_shared_if<8 * toff(e)>(g2, (m1 >> e) & 1);
-              });
-              static_for<0, CC>([&](auto i) {
-                constexpr int e = e0 + decltype(i)::value;
-                st_shared_if<8 * toff(e)>(g2, cadd(a[decltype(i)::value], cmulc(s2[toff(e)], v[e])), (m1 >> e) & 1);
-              });
-            });
+            }
+          };
+          if constexpr (kHalfSizes && (E / CC) % 2 == 0) {
+            if (half) corr(std::integral_constant<int, E / CC / 2>{});
+            else corr(std::integral_constant<int, E / CC>{});
+          } else {
+            corr(std::integral_constant<int, E / CC>{});
           }
         }
         sync();
