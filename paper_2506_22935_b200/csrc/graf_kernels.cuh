@@ -443,6 +443,32 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+// Inverse FFT of a band-limited row whose only nonzero slots are e = 0 and e = E - 1
+// (the loss band |d| < T = M/E; c4): the first pass's radix-E DFT of two nonzero inputs
+// is X[r] = x_0 + x_{E-1} W_E^{(E-1) r} (compile-time twiddles), the rest is fft_rows.
+template <int M, int E, class TW, class Sync>
+__device__ __forceinline__ void ifft_band_edges(float2 (&v)[E], float2* sh, int t, const TW& tw, const Sync& sync) {
+  constexpr int T = M / E;
+  static_assert(pass_radix(M, E, 0) == E && E <= Pad<E>::P, "first pass must be one radix-E butterfly");
+  const float2 x0 = v[0], xl = v[E - 1];
+  float2* b = sh + padded<E>(t * E);
+  static_for<0, E>([&](auto r) {
+    constexpr int K = ((E - 1) * decltype(r)::value) % E;
+    b[decltype(r)::value] = cadd(x0, twc<K, E, true>(xl));
+  });
+  sync();
+  if constexpr (PadStride<E, T>::AFFINE) {
+    const float2* c = sh + padded<E>(t);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = c[e * PadStride<E, T>::value];
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
+  }
+  sync();
+  fft_rows<M, E, 1, true>(v, sh, t, tw, sync);
+}
+
 // bits e of [e_lo, e_hi) as a mask over the E register slots
 __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi) {
   const unsigned long long hi = e_hi >= 64 ? ~0ull : ((1ull << e_hi) - 1ull);
@@ -494,6 +520,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // (compiled for M >= 2048 only: the extra code path measured 3 % slower at M = 1024)
   constexpr bool kHalfSizes = (M >= 2048) && !SPLIT;
   const bool half = kHalfSizes && !p.periodic && 2 * N <= M;
+  // loss band |d| <= d_max < T: a loss pass's cotangent G lives in slots e = 0 and E - 1
+  // only (M >= 2048, first pass one radix-E butterfly)
+  constexpr bool kEdgeBand = kHalfSizes && (KIND == K_ISL || KIND == K_PASS2 || KIND == K_MATCH) &&
+                             pass_radix(M, E, 0) == E && E <= GRAF_MAX_RADIX && num_passes(M, E) > 1;
+  const bool edge_band = kEdgeBand && p.d_max < T;
   // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
   const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * (NL + M) + NL + 1;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
@@ -937,7 +968,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       if constexpr (T < 32) do_adj = __any_sync(0xffffffffu, do_adj);
       if (do_adj) {
         stg_release();
-        row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
+        if constexpr (kEdgeBand) {
+          if (edge_band) ifft_band_edges<M, E>(v, sh, t, tw, sync);
+          else row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
+        } else {
+          row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
+        }
         // keep the correlation's loads below the last inverse pass
         asm volatile("" ::: "memory");
         // term 1 at p = n: g[n] += H[n] s[n-k];  term 2 at p = n-k: g[n-k] += conj(H[n]) s[n],
