@@ -525,6 +525,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   constexpr bool kEdgeBand = kHalfSizes && (KIND == K_ISL || KIND == K_PASS2 || KIND == K_MATCH) &&
                              pass_radix(M, E, 0) == E && E <= GRAF_MAX_RADIX && num_passes(M, E) > 1;
   const bool edge_band = kEdgeBand && p.d_max < T;
+  // ... and the loss epilogues, the band cache and (pass 1) the loss statistics then touch
+  // slots 0 and E - 1 only (the others are outside the band: their terms are 0)
+  const bool eb = FWD ? (kHalfSizes && p.d_max < T) : edge_band;
   // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
   const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * (NL + M) + NL + 1;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
@@ -691,6 +694,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       if (cread) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+          if (eb && e != 0 && e != E - 1) {
+            v[e] = make_float2(0.f, 0.f);
+            continue;
+          }
           const int m = t + e * T;
           const int d = m < M / 2 ? m : m - M;
           v[e] = (valid && ((band >> e) & 1)) ? crow[d] : make_float2(0.f, 0.f);
@@ -743,6 +750,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         // pass 1: keep the loss band of this row for pass 2
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+          if (eb && e != 0 && e != E - 1) continue;
           const int m = t + e * T;
           const int d = m < M / 2 ? m : m - M;
           if ((band >> e) & 1) crow[d] = v[e];
@@ -861,6 +869,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+          if (eb && e != 0 && e != E - 1) continue;   // outside the band: no term, G unused
           const bool in = (inm >> e) & 1;
           float w = 1.f;
           if constexpr (WGT) {
@@ -933,6 +942,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             float rowZ = 0.f, rowC = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
+              if (eb && e != 0 && e != E - 1) continue;
               const bool in = (inm >> e) & 1;
               const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
               const float x = p.normalize ? chi * invE2 : chi;
