@@ -25,6 +25,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 
 namespace graf {
 
@@ -171,6 +172,15 @@ __device__ __forceinline__ void dft(float2* x) {
 }
 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// compile-time loop: f(integral_constant<int, I>) for I in [B, E)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for_fft(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for_fft<B + 1, E>(f);
+  }
+}
 
 // exchange-buffer padding: one pad slot every max-radix elements (conflict-free
 // for every plan used; scripts/bank_sim.py)
@@ -422,6 +432,60 @@ __device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, cons
     }
     sync();
     fft_rows<M, E, P + 1, INV, Sync>(v, sh, t, tw, sync);
+  }
+}
+
+// Forward FFT of which only the outputs of slots 0 and E - 1 are needed (a loss band
+// narrower than T = M/E bins): the passes before the last run in full (their outputs
+// feed every thread through the exchange), the last pass evaluates only the two
+// butterfly outputs that land in slots 0 (q = 0, r = 0) and E - 1 (q = Q - 1, r = R - 1).
+// The other slots are left zero.  For last passes P >= 2 of uncached plans.
+template <int M, int E, int P>
+__device__ __forceinline__ void fft_last_edges(float2 (&v)[E], int t) {
+  constexpr int T = M / E;
+  constexpr int R = pass_radix(M, E, P);
+  constexpr int NS = pass_ns(M, E, P);
+  constexpr int Q = E / R;
+  static_assert(NS * R == M && NS > 1 && P >= 2 && !Twiddles<M, E>::CACHE, "last pass of an uncached plan");
+  float2 w[R];
+  // q = 0: X_0 = sum_r W^{r jm} x_r with jm = t (NS > T here since NS * R = M, R <= E)
+  tw_powers<R>(__ldg(&g_tw[(t & (NS - 1)) * (kMaxM / M)]), w);
+  float2 x0 = v[0];
+#pragma unroll
+  for (int r = 1; r < R; ++r) x0 = cadd(x0, cmul(v[r * Q], w[r]));
+  // q = Q - 1: X_{R-1} = sum_r W_R^{r (R-1)} W^{r jm} x_r with jm = t + (Q-1) T
+  if constexpr (Q > 1) tw_powers<R>(__ldg(&g_tw[((t + (Q - 1) * T) & (NS - 1)) * (kMaxM / M)]), w);
+  float2 xl = v[Q - 1];
+  static_for_fft<1, R>([&](auto rc) {
+    constexpr int r = decltype(rc)::value;
+    xl = cadd(xl, twc<(r * (R - 1)) % R, R, false>(cmul(v[(Q - 1) + r * Q], w[r])));
+  });
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
+  v[0] = x0;
+  v[E - 1] = xl;
+}
+
+template <int M, int E, int P, class Sync>
+__device__ __forceinline__ void fft_rows_edges(float2 (&v)[E], float2* sh, int t, const Twiddles<M, E>& tw,
+                                               const Sync& sync) {
+  constexpr int T = M / E;
+  constexpr int NP = num_passes(M, E);
+  if constexpr (P + 1 < NP) {
+    stockham_pass<M, E, P, false>(v, sh, t, tw);
+    sync();
+    if constexpr (PadStride<E, T>::AFFINE) {
+      const float2* b = sh + padded<E>(t);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = b[e * PadStride<E, T>::value];
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
+    }
+    sync();
+    fft_rows_edges<M, E, P + 1, Sync>(v, sh, t, tw, sync);
+  } else {
+    fft_last_edges<M, E, P>(v, t);
   }
 }
 

@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // ... and the loss epilogues, the band cache and (pass 1) the loss statistics then touch
   // slots 0 and E - 1 only (the others are outside the band: their terms are 0)
   const bool eb = FWD ? (kHalfSizes && p.d_max < T) : edge_band;
+  constexpr bool kEdgeFwd = kHalfSizes && FWD && num_passes(M, E) >= 3 && !Twiddles<C::MX, E2>::CACHE;
   // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
   const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * (NL + M) + NL + 1;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
@@ -742,9 +743,15 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
         }
       }
-      // ---- a2: forward Doppler FFT
+      // ---- a2: forward Doppler FFT (a loss pass over a band narrower than T bins with
+      //      no surface output needs slots 0 and E - 1 only: the last pass is pruned)
       stg_release();
-      row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
+      if constexpr (kEdgeFwd) {
+        if (eb && p.surface == nullptr) fft_rows_edges<M, E, 0>(v, sh, t, tw, sync);
+        else row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
+      } else {
+        row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
+      }
       asm volatile("" ::: "memory");
       if (FWD && p.cache == 1 && lrow) {
         // pass 1: keep the loss band of this row for pass 2
