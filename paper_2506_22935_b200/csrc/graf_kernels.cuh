@@ -724,23 +724,20 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const float2* a = sv + 2 * t;
         const float2* c = sv2 + 2 * t - k;
         const float4* a4 = reinterpret_cast<const float4*>(a);
-        if ((k & 1) == 0) {
-          const float4* c4 = reinterpret_cast<const float4*>(c);
+        // (odd k: the shifted copy holds s[2t - k + 2eT] at an even, aligned, position)
+        const float4* c4 = reinterpret_cast<const float4*>((k & 1) == 0 ? c : sv_o + 2 * t - k);
 #pragma unroll
-          for (int e = 0; e < E2; ++e) {
-            const float4 x = a4[e * T], y = c4[e * T];
-            v[e] = cmulc(make_float2(x.x, x.y), make_float2(y.x, y.y));
-            v[e + E2] = cmulc(make_float2(x.z, x.w), make_float2(y.z, y.w));
+        for (int e = 0; e < E2; ++e) {
+          // pairs outside the row's support [lo, hi) are zero: no loads (about half of
+          // the pairs of a full-plane row)
+          if ((((vmask >> e) | (vmask >> (e + E2))) & 1) == 0) {
+            v[e] = make_float2(0.f, 0.f);
+            v[e + E2] = make_float2(0.f, 0.f);
+            continue;
           }
-        } else {
-          // odd k: the shifted copy holds s[2t - k + 2eT] at an even (aligned) position
-          const float4* c4 = reinterpret_cast<const float4*>(sv_o + 2 * t - k);
-#pragma unroll
-          for (int e = 0; e < E2; ++e) {
-            const float4 x = a4[e * T], y = c4[e * T];
-            v[e] = cmulc(make_float2(x.x, x.y), make_float2(y.x, y.y));
-            v[e + E2] = cmulc(make_float2(x.z, x.w), make_float2(y.z, y.w));
-          }
+          const float4 x = a4[e * T], y = c4[e * T];
+          v[e] = cmulc(make_float2(x.x, x.y), make_float2(y.x, y.y));
+          v[e + E2] = cmulc(make_float2(x.z, x.w), make_float2(y.z, y.w));
         }
       }
       // ---- a2: forward Doppler FFT (a loss pass over a band narrower than T bins with
@@ -1048,6 +1045,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             const float2* s1 = sv2 + tb - k;
             static_for<0, E2 / CP>([&](auto c) {
               constexpr int j0 = decltype(c)::value * CP;
+              constexpr VMask cbits = (((VMask)1 << CP) - 1) << j0;
+              if ((m1 & (cbits | (cbits << E2))) == 0) return;   // no slot of this chunk in the support
               float2 a[2 * CP], sl[2 * CP];
               static_for<0, CP>([&](auto i) {
                 constexpr int j = j0 + decltype(i)::value;
@@ -1076,6 +1075,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             const float4* s2 = reinterpret_cast<const float4*>(sv + tb);
             static_for<0, E2 / CP>([&](auto c) {
               constexpr int j0 = decltype(c)::value * CP;
+              constexpr VMask cbits = (((VMask)1 << CP) - 1) << j0;
+              if ((m1 & (cbits | (cbits << E2))) == 0) return;
               float2 a[2 * CP];
               float4 q[CP];
               static_for<0, CP>([&](auto i) {
