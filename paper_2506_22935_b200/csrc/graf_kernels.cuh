@@ -1107,6 +1107,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               const float2* s1 = sv2 + tb - k;
               static_for<0, NCH>([&](auto c) {
                 constexpr int e0 = decltype(c)::value * CC;
+                if ((m1 & ((((VMask)1 << CC) - 1) << e0)) == 0) return;   // chunk outside the support
                 float2 a[CC];
                 static_for<0, CC>([&](auto i) {
                   constexpr int e = e0 + decltype(i)::value;
@@ -1125,6 +1126,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               const float2* s2 = sv + tb;
               static_for<0, NCH>([&](auto c) {
                 constexpr int e0 = decltype(c)::value * CC;
+                if ((m1 & ((((VMask)1 << CC) - 1) << e0)) == 0) return;   // chunk outside the support
                 float2 a[CC];
                 static_for<0, CC>([&](auto i) {
                   constexpr int e = e0 + decltype(i)::value;
