@@ -171,6 +171,28 @@ __device__ __forceinline__ void dft(float2* x) {
   }
 }
 
+// DFT of length R whose inputs x[NZ..R) are zero (a zero-padded row's first pass):
+// the same radix-2 decimation as dft<R> with the all-zero branches folded away
+template <int R, int NZ, bool INV>
+__device__ __forceinline__ void dft_lz(float2* x) {
+  if constexpr (NZ >= R) {
+    dft<R, INV>(x);
+  } else if constexpr (NZ <= 1) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) x[r] = x[0];   // DFT of (a, 0, ..., 0)
+  } else {
+    float2 e[R / 2], o[R / 2];
+#pragma unroll
+    for (int i = 0; i < R / 2; ++i) {
+      e[i] = x[2 * i];
+      o[i] = x[2 * i + 1];
+    }
+    dft_lz<R / 2, (NZ + 1) / 2, INV>(e);
+    dft_lz<R / 2, NZ / 2, INV>(o);
+    dft_combine<0, R, INV>(x, e, o);
+  }
+}
+
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
 // compile-time loop: f(integral_constant<int, I>) for I in [B, E)
@@ -466,13 +488,21 @@ __device__ __forceinline__ void fft_last_edges(float2 (&v)[E], int t) {
   v[E - 1] = xl;
 }
 
-template <int M, int E, int P, class Sync>
+template <int M, int E, int P, bool HZ, class Sync>
 __device__ __forceinline__ void fft_rows_edges(float2 (&v)[E], float2* sh, int t, const Twiddles<M, E>& tw,
                                                const Sync& sync) {
   constexpr int T = M / E;
   constexpr int NP = num_passes(M, E);
   if constexpr (P + 1 < NP) {
-    stockham_pass<M, E, P, false>(v, sh, t, tw);
+    if constexpr (P == 0 && HZ && pass_radix(M, E, 0) == E && E <= Pad<E>::P) {
+      // zero-padded row (2N <= M): the first butterfly's inputs v[E/2..E) are zero
+      dft_lz<E, E / 2, false>(v);
+      float2* b = sh + padded<E>(t * E);
+#pragma unroll
+      for (int r = 0; r < E; ++r) b[r] = v[r];
+    } else {
+      stockham_pass<M, E, P, false>(v, sh, t, tw);
+    }
     sync();
     if constexpr (PadStride<E, T>::AFFINE) {
       const float2* b = sh + padded<E>(t);
@@ -483,7 +513,7 @@ __device__ __forceinline__ void fft_rows_edges(float2 (&v)[E], float2* sh, int t
       for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
     }
     sync();
-    fft_rows_edges<M, E, P + 1, Sync>(v, sh, t, tw, sync);
+    fft_rows_edges<M, E, P + 1, HZ, Sync>(v, sh, t, tw, sync);
   } else {
     fft_last_edges<M, E, P>(v, t);
   }

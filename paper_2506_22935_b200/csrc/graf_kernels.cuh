@@ -744,7 +744,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       //      no surface output needs slots 0 and E - 1 only: the last pass is pruned)
       stg_release();
       if constexpr (kEdgeFwd) {
-        if (eb && p.surface == nullptr) fft_rows_edges<M, E, 0>(v, sh, t, tw, sync);
+        if (eb && p.surface == nullptr) {
+          if (half) fft_rows_edges<M, E, 0, true>(v, sh, t, tw, sync);
+          else fft_rows_edges<M, E, 0, false>(v, sh, t, tw, sync);
+        }
         else row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
       } else {
         row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
