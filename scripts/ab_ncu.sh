@@ -1,3 +1,6 @@
+#!/bin/bash
+# ncu A/B of a variant library (vlib/libgraf_f2.so, built with scripts/ab_lib.sh conventions) against
+# the in-tree one on c5/c4/c2; run under gpurun.  Development tool.
 mkdir -p gpurun_out
 for c in 5 4 2; do
  for L in "" vlib/libgraf_f2.so; do
