@@ -100,3 +100,31 @@ def test_fuzz_backward(case):
     G = dA[0] if layout == "raw" else np.roll(dA[0], -(M // 2), axis=1)
     ref = O.adjoint(s[0], M, G.astype(np.complex128), rows, periodic=periodic)
     assert np.abs(g - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-30), (case, N, M, periodic, kb, ke, layout)
+
+
+@pytest.mark.parametrize("case", range(32))
+def test_fuzz_large_m_narrow_band(case):
+    # M = 2048 ... 8192 (the sizes that compile the band-edge and zero-padded paths), N up
+    # to M, loss bands mostly narrower than M/16 bins, every loss kind of the fused kernels
+    r = SplitMix64(0xBA4D0000 + case)
+    M = 2048 << randint(r, 0, 2)
+    N = randint(r, 2, min(M, 1200))
+    T = M // 16
+    d_max = randint(r, 0, T - 1) if r.uniform(1)[0] < 0.7 else randint(r, T, M // 2)
+    ml_d = min(randint(r, 0, 2), d_max)
+    if d_max == ml_d:
+        ml_d = max(0, d_max - 1)
+    k_max = randint(r, 1, min(N - 1, 200)) if N > 1 else 1
+    lam_psl = [0.0, 1.0][randint(r, 0, 1)]
+    spec = dict(k_max=k_max, d_max=d_max, ml_k=0, ml_d=ml_d, lambda_isl=1.0, lambda_psl=lam_psl,
+                temperature=[0.02, 0.05][randint(r, 0, 1)], normalize=1)
+    s = np.stack([complex_gaussian(SplitMix64(case * 77 + b), N) for b in range(2)])
+    loss, g, _ = graf.af_loss_grad(dev(s), M, graf.LossSpec.from_dict(spec))
+    loss, g = loss.cpu().numpy(), g.cpu().numpy()
+    ospec = O.LossSpec.from_dict(spec)
+    for b in range(2):
+        L_ref, g_ref, t = O.loss_and_grad(s[b], M, ospec)
+        ctx = (case, N, M, spec, b)
+        assert abs(loss[b] - L_ref) <= 1e-4 * abs(L_ref) + 1e-30, (ctx, loss[b], L_ref)
+        tol = 1e-4 * max(np.abs(g_ref).max(), t["sigma_g"])
+        assert np.abs(g[b] - g_ref).max() <= tol + 1e-30, (ctx, np.abs(g[b] - g_ref).max(), tol)
