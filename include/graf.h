@@ -29,7 +29,11 @@
  *    L219): dL/dRe s = 2 Re g, dL/dIm s = 2 Im g.  Outputs are overwritten,
  *    never accumulated.  Torch's complex .grad equals 2*g.
  *  - Reentrant: no mutable global state except an immutable per-device table
- *    of M-th roots of unity, initialised once per device on first use.
+ *    of M-th roots of unity.  It is filled by a small kernel enqueued on the
+ *    stream of the first call on a device (or of graf_init); calls on other
+ *    streams are ordered after it with an event wait, and a first call made
+ *    inside CUDA-graph capture records the fill into the graph.  No call ever
+ *    blocks the host or synchronises the device.
  *  - Deterministic: fixed reduction order, no floating-point atomics; a call
  *    repeated on the same inputs returns bitwise-identical outputs.
  *  - Errors: argument checks happen on the host before any launch and return a
@@ -48,7 +52,7 @@
 extern "C" {
 #endif
 
-#define GRAF_ABI_VERSION 5
+#define GRAF_ABI_VERSION 6
 #define GRAF_MAX_M 16384
 
 typedef enum {
@@ -56,7 +60,7 @@ typedef enum {
   GRAF_EINVAL = 1,        /* malformed argument (sizes, ranges, NULL, alignment) */
   GRAF_EUNSUPPORTED = 2,  /* well-formed but outside v1 device limits (M > 16384, M < N, ...) */
   GRAF_ECUDA = 3,         /* a CUDA runtime call or launch failed */
-  GRAF_ENONFINITE = 4,    /* reserved (debug scans) */
+  /* 4 is unused: value-dependent problems are never detected (no host sync), see above */
   GRAF_EWORKSPACE = 5     /* ws_bytes < graf_workspace_bytes(...) */
 } graf_status;
 
@@ -89,6 +93,13 @@ typedef struct {
                                Alg. 1's two-axis fftshift, L252).  The loss region uses the
                                circular delay distance min(k mod N, N - k mod N) <= k_max and
                                weights w_k[k + N - 1] for k in (-N/2, N/2].  (ABI v2) */
+  const int32_t* skip;      /* nullable device int32 [B]: waveforms b with skip[b] != 0 are not
+                               computed, and every per-waveform output of theirs (surface rows,
+                               partials, loss, grad) is left untouched.  A guarded re-run of a
+                               batch (the sharded single pass's fallback) costs nothing for the
+                               skipped waveforms and needs no host-side decision.  Honoured by
+                               graf_af_forward / _loss_grad / _backward; the sp_* and xaf_* entry
+                               points return GRAF_EUNSUPPORTED when it is set.  (ABI v6) */
 } graf_af_desc;
 
 /* Loss over the sidelobe region Omega_s (never defined by the paper,
@@ -132,6 +143,11 @@ int32_t graf_abi_version(void);
 const char* graf_status_string(graf_status status);
 const char* graf_last_error(void);
 
+/* Optional explicit initialisation of the current device: enqueues the fill of the
+ * roots-of-unity table on `stream` (the first entry-point call does the same when it
+ * has not happened).  Never blocks.  (ABI v6) */
+graf_status graf_init(void* stream);
+
 /* Bytes of device workspace the call with these descriptors needs (0 on
  * invalid descriptors).  Same value for graf_af_forward, graf_af_loss_grad and
  * graf_af_backward with the same descriptors; loss may be NULL. */
@@ -150,7 +166,11 @@ graf_status graf_af_forward(const graf_af_desc* af, const graf_loss_desc* loss,
  * this shard's share of the normalization term, so the SUM over shards is the
  * full gradient.  Optionally writes the surface window too (af->out_kind).
  * ISL-only losses (lambda_psl == 0) run as ONE fused pass (forward, epilogue,
- * inverse FFT, delay correlation); soft-PSL needs the global LSE and runs two. */
+ * inverse FFT, delay correlation); soft-PSL needs the global LSE and runs two.
+ * Sharded calls without `global`: the loss is this shard's part of a sum over shards
+ * (ISL and match terms are linear in the rows).  A shard that owns no loss rows writes
+ * grad 0 and loss 0 then; with soft-PSL or hard-PSL terms, which need the global
+ * statistic, `global` is required (GRAF_EINVAL before any launch otherwise). */
 graf_status graf_af_loss_grad(const graf_af_desc* af, const graf_loss_desc* loss,
                               const void* s, const graf_partials* global,
                               double* loss_out, void* grad, void* surface,
@@ -212,8 +232,10 @@ graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void
                               void* grad1, void* grad2, void* ws, size_t ws_bytes, void* stream);
 
 /* Spectral variance of each waveform (the paper's section-7 LPI term, L417):
- *   SV_b = var{ |F s_b|^2 / sum |F s_b|^2 } over the N DFT bins, unbiased (N - 1;
- *   the paper's PyTorch var, reading R22), F the length-N DFT,
+ *   SV_b = var{ |F s_b|^2 / sum |F s_b|^2 } over the N DFT bins, F the length-N DFT,
+ *   var = sum (p - mean p)^2 / (N - ddof): ddof = 0 population variance (SPEC.md L328,
+ *   the default of the binding; reading R22), ddof = 1 the unbiased estimator (PyTorch's
+ *   var default).  (ABI v6)
  * and its Wirtinger gradient dSV/ds*.  Writes weight*SV_b into loss[b] and
  * weight*dSV/ds* into grad[b][:], or ADDS them when accumulate = 1 (to combine
  * with a graf_af_loss_grad result: the Eq. 26 loss PSL + lambda*alpha*SV).
@@ -223,7 +245,7 @@ graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void
  * 2 <= N <= 16384.  No workspace. */
 graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, float weight,
                                    const float* weights, double* loss, void* grad, int32_t accumulate,
-                                   void* stream);
+                                   int32_t ddof, void* stream);
 
 /* Differentiable mainlobe width:
  *   W_b = sum_tau |tau| sigma(gamma (chi(tau,0) - chi(0,0)/2))

@@ -302,13 +302,21 @@ def loss_and_grad_chunked(s: np.ndarray, M: int, spec: LossSpec, chunk_rows: int
     E = energy(s)
     T = spec.temperature
     S, c, Z, cnt = 0.0, -np.inf, 0.0, 0
+    # the DFT-matrix blocks are the same for every row chunk: built once (same values)
+    cache = {}
+
+    def W(b0, sign=-1):
+        key = (b0, sign)
+        if key not in cache:
+            cache[key] = dft_matrix(n, M, bins[b0:b0 + chunk_bins], sign=sign)
+        return cache[key]
+
     # sweep 1
     for r0 in range(0, len(rows_all), chunk_rows):
         rows = rows_all[r0:r0 + chunk_rows]
         Rm = lag_products(s, rows)
         for b0 in range(0, len(bins), chunk_bins):
-            bb = bins[b0:b0 + chunk_bins]
-            A = Rm @ dft_matrix(n, M, bb)
+            A = Rm @ W(b0)
             chi = A.real ** 2 + A.imag ** 2
             x = chi / E ** 2 if spec.normalize else chi
             msk = mask_all[r0:r0 + chunk_rows, b0:b0 + chunk_bins]
@@ -333,8 +341,7 @@ def loss_and_grad_chunked(s: np.ndarray, M: int, spec: LossSpec, chunk_rows: int
         Rm = lag_products(s, rows)
         H = np.zeros((len(rows), n), dtype=np.complex128)
         for b0 in range(0, len(bins), chunk_bins):
-            bb = bins[b0:b0 + chunk_bins]
-            A = Rm @ dft_matrix(n, M, bb)
+            A = Rm @ W(b0)
             chi = A.real ** 2 + A.imag ** 2
             x = chi / E ** 2 if spec.normalize else chi
             msk = mask_all[r0:r0 + chunk_rows, b0:b0 + chunk_bins]
@@ -343,7 +350,7 @@ def loss_and_grad_chunked(s: np.ndarray, M: int, spec: LossSpec, chunk_rows: int
             fchi += float(np.sum(fp * chi))
             afchi += float(np.sum(np.abs(fp) * chi))
             G = fp * A / E ** 2 if spec.normalize else fp * A
-            H += G @ dft_matrix(n, M, bb, sign=+1).T
+            H += G @ W(b0, +1).T
         g += correlate(s, H, rows)
     if spec.normalize:
         g = g - (2.0 / E ** 3) * fchi * s
@@ -396,10 +403,12 @@ def hard_psl_and_grad(s: np.ndarray, M: int, spec: LossSpec, periodic: bool = Fa
     return psl, g, (int(rows[i]), int(bins[j]))
 
 
-def spectral_variance_and_grad(s: np.ndarray):
-    """SV = var{|F s|^2 / sum |F s|^2} over the N DFT bins (the paper's
-    PyTorch var: unbiased, N - 1 in the denominator, reading R22), F = length-N DFT
-    written as its matrix; and dSV/ds* (chain rule through p_j = |S_j|^2 / P)."""
+def spectral_variance_and_grad(s: np.ndarray, ddof: int = 0):
+    """SV = var{|F s|^2 / sum |F s|^2} over the N DFT bins, F = length-N DFT
+    written as its matrix; and dSV/ds* (chain rule through p_j = |S_j|^2 / P).
+    var = sum (p - mean p)^2 / (N - ddof): ddof = 0 is the population variance that
+    SPEC.md L328 fixes (all-ones N = 4 -> 3/16; reading R22), ddof = 1 the
+    unbiased estimator (PyTorch's var default)."""
     s = np.asarray(s, dtype=np.complex128)
     n = s.shape[0]
     F = dft_matrix(n, n, np.arange(n)).T          # S_j = sum_n s_n exp(-2 pi i j n / N)
@@ -408,8 +417,8 @@ def spectral_variance_and_grad(s: np.ndarray):
     P = float(np.sum(pw))
     p = pw / P
     mean = float(np.mean(p))
-    sv = float(np.sum((p - mean) ** 2) / (n - 1))
-    c = 2.0 * (p - mean) / (n - 1)                # dSV/dp_j
+    sv = float(np.sum((p - mean) ** 2) / (n - ddof))
+    c = 2.0 * (p - mean) / (n - ddof)             # dSV/dp_j
     dS = (c - float(np.sum(c * p))) * S / P       # dSV/dS_j*
     g = np.conj(F).T @ dS                         # adjoint of S = F s
     return sv, g

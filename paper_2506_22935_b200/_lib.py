@@ -10,8 +10,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # GRAF_LIB_PATH: tuning builds only (scripts/tune.py); the default is the in-tree library.
 LIB_PATH = os.environ.get("GRAF_LIB_PATH") or os.path.join(PKG, "libgraf.so")
 
-ABI_VERSION = 5
-GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_ENONFINITE, GRAF_EWORKSPACE = range(6)
+ABI_VERSION = 6
+GRAF_OK, GRAF_EINVAL, GRAF_EUNSUPPORTED, GRAF_ECUDA, GRAF_EWORKSPACE = 0, 1, 2, 3, 5
 OUT_NONE, OUT_C64, OUT_ABS_F32, OUT_POW_F32 = range(4)
 DOPPLER_RAW, DOPPLER_CENTERED = 0, 1
 
@@ -20,14 +20,15 @@ EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_wo
            "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
            "graf_phase_adam_step", "graf_xaf_workspace_bytes", "graf_xaf_forward", "graf_xaf_loss_grad",
            "graf_xaf_backward", "graf_mainlobe_width", "graf_af_single_pass_eligible",
-           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end")
+           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end", "graf_init")
 
 
 class AfDesc(ctypes.Structure):
     _fields_ = [("abi_version", c_int32), ("n", c_int32), ("m", c_int32), ("out_kind", c_int32),
                 ("batch", c_int64), ("k_begin", c_int32), ("k_end", c_int32),
                 ("doppler_layout", c_int32), ("normalize_output", c_int32),
-                ("shard_index", c_int32), ("shard_count", c_int32), ("periodic", c_int32)]
+                ("shard_index", c_int32), ("shard_count", c_int32), ("periodic", c_int32),
+                ("skip", c_void_p)]
 
 
 class LossDesc(ctypes.Structure):
@@ -102,7 +103,9 @@ def lib() -> ctypes.CDLL:
                                           c_int32, c_void_p]
         L.graf_spectral_variance.restype = c_int32
         L.graf_spectral_variance.argtypes = [c_int64, c_int32, c_void_p, c_float, c_void_p, c_void_p, c_void_p,
-                                             c_int32, c_void_p]
+                                             c_int32, c_int32, c_void_p]
+        L.graf_init.restype = c_int32
+        L.graf_init.argtypes = [c_void_p]
         L.graf_phase_adam_step.restype = c_int32
         L.graf_phase_adam_step.argtypes = [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                            c_void_p, c_float, c_float, c_float, c_float, c_void_p]

@@ -18,8 +18,8 @@
 
 namespace graf {
 thread_local int t_launches = 0;   // kernels / memsets enqueued by this thread's last entry-point call
-std::vector<TwUpload>& tw_uploaders() {
-  static std::vector<TwUpload> v;   // filled by the row-kernel translation units at load time
+std::vector<TwFill>& tw_fillers() {
+  static std::vector<TwFill> v;   // filled by the row-kernel translation units at load time
   return v;
 }
 namespace {
@@ -59,30 +59,59 @@ graf_status cuda_fail(cudaError_t e, const char* what) {
 }
 
 // ---------------------------------------------------------------------------
-// one-time per-device twiddle table (immutable afterwards)
+// per-device twiddle table (immutable once filled).  The fill is a kernel per
+// translation unit, enqueued on the stream of the first call (never a host-blocking
+// copy).  State per device: 0 not filled, 1 fill enqueued on `st` (event `ev`
+// recorded after it), 2 known complete.  A call on another stream while the fill is
+// in flight waits on `ev` (device-side); a call inside CUDA-graph capture that cannot
+// prove the fill complete records its own (idempotent) fill into the graph.
 // ---------------------------------------------------------------------------
-std::once_flag g_tw_once[kMaxDev];
-cudaError_t g_tw_err[kMaxDev];
+struct TwState {
+  std::mutex mu;
+  int state = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+TwState g_tws[kMaxDev];
 
-cudaError_t ensure_twiddles() {
+cudaError_t fill_all_twiddles(cudaStream_t st) {
+  cudaError_t e = launch_tw_init(st);   // this unit's copy (graf_fft.cuh)
+  for (auto f : tw_fillers())
+    if (e == cudaSuccess) e = f(st);
+  if (e == cudaSuccess) t_launches += 1 + (int)tw_fillers().size();
+  return e;
+}
+
+cudaError_t ensure_twiddles(cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
-  std::call_once(g_tw_once[dev], [dev] {
-    std::vector<float2> h(kMaxM);
-    for (int i = 0; i < kMaxM; ++i) {
-      // exp(-2 pi i * i / kMaxM) from exact integer phases, rounded once to float
-      const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)i / kMaxM;
-      h[i] = make_float2((float)cosl(a), (float)sinl(a));
+  TwState& s = g_tws[dev];
+  std::lock_guard<std::mutex> lk(s.mu);
+  if (s.state == 2) return cudaSuccess;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if ((e = cudaStreamIsCapturing(st, &cs)) != cudaSuccess) return e;
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (s.state == 1) {
+    if (st == s.st) return cudaSuccess;               // stream-ordered after the fill
+    if (capturing) return fill_all_twiddles(st);      // the graph carries its own fill
+    const cudaError_t q = cudaEventQuery(s.ev);
+    if (q == cudaSuccess) {
+      s.state = 2;
+      return cudaSuccess;
     }
-    // every translation unit holds its own copy of the table (graf_fft.cuh)
-    cudaError_t e0 = cudaMemcpyToSymbol(g_tw, h.data(), sizeof(float2) * kMaxM);
-    for (auto up : tw_uploaders())
-      if (e0 == cudaSuccess) e0 = up(h.data());
-    g_tw_err[dev] = e0;
-  });
-  return g_tw_err[dev];
+    if (q != cudaErrorNotReady) return q;
+    (void)cudaGetLastError();                         // NotReady is a status, not an error
+    return cudaStreamWaitEvent(st, s.ev, 0);
+  }
+  if ((e = fill_all_twiddles(st)) != cudaSuccess) return e;
+  if (capturing) return cudaSuccess;                  // not marked: the fill runs at replay
+  if (!s.ev && (e = cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(s.ev, st)) != cudaSuccess) return e;
+  s.st = st;
+  s.state = 1;
+  return cudaSuccess;
 }
 
 struct CfgInfo {
@@ -286,7 +315,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   // actual P <= bound from the kernel's measured occupancy (choose_P).
   const long long B = af->batch;
   const long long maxP = std::max(1, (pl.U + ci.S - 1) / ci.S);
-  const long long capP = std::max(1LL, (long long)(kNumSM * 8 + B - 1) / B);
+  const long long capP = std::max(1LL, (long long)(device_sm_count() * 8 + B - 1) / B);
   pl.P = (int)std::max(1LL, std::min(maxP, capP));
   pl.Pbound = pl.P;
   size_t off = 0;
@@ -404,6 +433,7 @@ RowParams base_params(const graf_af_desc* af, const void* s, const Plan& pl, voi
     rp.s2 = static_cast<const float2*>(cx.s2);
     rp.gpart2 = rp.gpart + (size_t)af->batch * pl.Pbound * af->n;
   }
+  rp.skip = af->skip;
   rp.s_pad = pl.s_smem ? nullptr : reinterpret_cast<const float2*>(w + pl.off_spad);
   rp.s_pad1 = pl.s_smem ? nullptr : rp.s_pad + spad_elems(af->batch, af->n, af->m);
   return rp;
@@ -481,6 +511,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
   }
   f.loss = loss;
   f.grad = static_cast<float2*>(grad);
+  f.skip = af->skip;
   if (pl.cross) {
     f.s2 = static_cast<const float2*>(cx.s2);
     f.gpart2 = f.gpart + (size_t)af->batch * pl.Pbound * af->n;
@@ -497,6 +528,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
     fc.one = one ? one + b0 : nullptr;
     fc.loss = loss ? loss + b0 : nullptr;
     fc.grad = grad ? f.grad + b0 * af->n : nullptr;
+    fc.skip = f.skip ? f.skip + b0 : nullptr;
     if (f.s2) {
       fc.s2 = f.s2 + b0 * af->n;
       fc.gpart2 = f.gpart2 + b0 * pl.P * (long long)af->n;
@@ -522,6 +554,7 @@ graf_status run_partials_reduce(const graf_af_desc* af, const graf_loss_desc* L,
   r.out = out;
   r.onepass = onepass;
   r.xbar = xbar;
+  r.skip = af->skip;
   partials_reduce_kernel<<<(r.B + 3) / 4, 128, 0, st>>>(r);   // a warp per waveform
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) ++t_launches;
@@ -532,6 +565,7 @@ graf_status check_cross(const graf_af_desc* af, const graf_loss_desc* L, const v
   if (!s2 || !aligned8(s2)) return fail(GRAF_EINVAL, "s2 is NULL or not 8-byte aligned");
   if (af->periodic) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity is aperiodic in v1");
   if (af->shard_count > 1) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity is unsharded in v1");
+  if (af->skip) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity: af->skip is not supported");
   if (af->m > 4096) return fail(GRAF_EUNSUPPORTED, "cross-ambiguity needs M <= 4096 in v1");
   if (L && (L->lambda_hpsl != 0.f || L->lambda_match != 0.f || L->w_k || L->w_d))
     return fail(GRAF_EUNSUPPORTED, "cross-ambiguity losses: unweighted ISL and soft-PSL in v1");
@@ -558,6 +592,7 @@ graf_status run_psl(const graf_af_desc* af, const graf_loss_desc* L, const Plan&
   q.accumulate = accumulate;
   q.loss = loss_out;
   q.grad = static_cast<float2*>(grad);
+  q.skip = af->skip;
   psl_grad_kernel<<<(unsigned)af->batch, 256, 0, st>>>(q);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "psl_grad_kernel launch");
@@ -574,13 +609,18 @@ extern "C" {
 
 int32_t graf_abi_version(void) { return GRAF_ABI_VERSION; }
 
+graf_status graf_init(void* stream) {
+  t_launches = 0;
+  const cudaError_t e = ensure_twiddles(static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GRAF_OK : cuda_fail(e, "twiddle table init");
+}
+
 const char* graf_status_string(graf_status s) {
   switch (s) {
     case GRAF_OK: return "GRAF_OK";
     case GRAF_EINVAL: return "GRAF_EINVAL: invalid argument";
     case GRAF_EUNSUPPORTED: return "GRAF_EUNSUPPORTED: outside v1 device limits";
     case GRAF_ECUDA: return "GRAF_ECUDA: CUDA error";
-    case GRAF_ENONFINITE: return "GRAF_ENONFINITE: non-finite value";
     case GRAF_EWORKSPACE: return "GRAF_EWORKSPACE: workspace too small";
     default: return "GRAF_UNKNOWN";
   }
@@ -609,7 +649,7 @@ static graf_status impl_forward(const CallCtx& cx, const graf_af_desc* af, const
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   if (reinterpret_cast<uintptr_t>(surface) & 15u) pl.bulk_ok = false;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  cudaError_t e = ensure_twiddles();
+  cudaError_t e = ensure_twiddles(cs);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   if (pl.U > 0 && (e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
   RowParams rp = base_params(af, s, pl, ws, cx);
@@ -644,15 +684,23 @@ static graf_status impl_loss_grad(const CallCtx& cx, const graf_af_desc* af, con
   Plan pl = make_plan(af, loss, Kind::LossGrad, cx.cross());
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   if (reinterpret_cast<uintptr_t>(surface) & 15u) pl.bulk_ok = false;
+  const bool needs_global = loss->lambda_psl != 0.f || loss->lambda_hpsl != 0.f;
+  if (pl.U == 0 && !global && needs_global)
+    return fail(GRAF_EINVAL, "a shard with no loss rows needs `global` for soft-PSL / hard-PSL losses");
+  if (loss->lambda_match != 0.f && global)
+    return fail(GRAF_EUNSUPPORTED, "match loss with global partials (v1: unsharded)");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  cudaError_t e = ensure_twiddles();
+  cudaError_t e = ensure_twiddles(cs);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   if (pl.U == 0) {
-    e = cudaMemsetAsync(grad, 0, sizeof(float2) * (size_t)af->batch * af->n, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "zero grad");
+    // no rows here: grad 0; a loss that is a sum over rows (ISL, match) is 0 too, else it
+    // comes from the global partials below (finalize with no partial records)
+    const bool zero_loss = loss_out && !global;
+    const long long tot = af->batch * (long long)af->n;
+    zero_outputs_kernel<<<(unsigned)std::min<long long>((tot + 255) / 256, 148 * 8), 256, 0, cs>>>(
+        static_cast<float2*>(grad), zero_loss ? loss_out : nullptr, af->batch, af->n, af->skip);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "zero_outputs_kernel launch");
     ++t_launches;
-    if (loss_out && !global) return fail(GRAF_EINVAL, "shard with no rows cannot compute the loss without `global`");
-    // loss from global partials via the finalize path with P partial records absent
   }
   if (pl.U > 0 && (e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
   RowParams rp = base_params(af, s, pl, ws, cx);
@@ -664,7 +712,6 @@ static graf_status impl_loss_grad(const CallCtx& cx, const graf_af_desc* af, con
   const bool soft = loss->lambda_psl != 0.f;
   const bool match = loss->lambda_match != 0.f;    // match loss, reading R24
   const bool dense = loss->lambda_isl != 0.f || soft || match;   // terms with a per-cell f'
-  if (match && global) return fail(GRAF_EUNSUPPORTED, "match loss with global partials (v1: unsharded)");
   if (match && !hpsl) {
     // one pass: f' = lambda_isl w + lambda_match (2x - t1 - t2) is known per cell
     if (pl.U > 0) {
@@ -695,7 +742,11 @@ static graf_status impl_loss_grad(const CallCtx& cx, const graf_af_desc* af, con
     // full-plane centred soft-PSL (reading R13): one optimistic pass with f' = lambda
     // expm1((x - xbar)/T), then guarded fallback passes that only run the waveforms whose
     // single pass is outside the R13 validity rule (max x - xbar > 40 T)
-    static const bool kOnePass = std::getenv("GRAF_NO_ONEPASS") == nullptr;
+#ifdef GRAF_NO_ONEPASS   // A/B builds only
+    constexpr bool kOnePass = false;
+#else
+    constexpr bool kOnePass = true;
+#endif
     const bool onepass = kOnePass && !stats && rp.centred && !hpsl && !match && !use_cache &&
                          rp.surface == nullptr && rp.shard_count <= 1 && pl.U > 0;
     if (onepass) {
@@ -777,6 +828,7 @@ static graf_status sp_common(const graf_af_desc* af, const graf_loss_desc* L, co
   if (!sp_eligible(af, L))
     return fail(GRAF_EUNSUPPORTED, "sharded single pass: only the full-plane, normalised, unweighted soft-PSL "
                                    "(graf_af_single_pass_eligible)");
+  if (af->skip) return fail(GRAF_EUNSUPPORTED, "sharded single pass: af->skip is not supported");
   *pl = make_plan(af, L, Kind::LossGrad, false);
   return check_ws(*pl, ws, ws_bytes);
 }
@@ -789,7 +841,7 @@ static graf_status impl_sp_begin(const graf_af_desc* af, const graf_loss_desc* L
   if (st) return st;
   if (!partials || (reinterpret_cast<uintptr_t>(partials) & 7u)) return fail(GRAF_EINVAL, "partials is NULL or misaligned");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  cudaError_t e = ensure_twiddles();
+  cudaError_t e = ensure_twiddles(cs);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   RowParams rp = base_params(af, s, pl, ws, CallCtx{});
   fill_loss(rp, af, L);
@@ -875,7 +927,7 @@ static graf_status impl_backward(const CallCtx& cx, const graf_af_desc* af, cons
   Plan pl = make_plan(af, nullptr, Kind::Backward, cx.cross());
   if ((st = check_ws(pl, ws, ws_bytes))) return st;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  cudaError_t e = ensure_twiddles();
+  cudaError_t e = ensure_twiddles(cs);
   if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   if ((e = prepare_spad(pl, af, s, ws, cs)) != cudaSuccess) return cuda_fail(e, "pad_s_kernel");
   RowParams rp = base_params(af, s, pl, ws, cx);
@@ -1013,18 +1065,19 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
 
 graf_status graf_spectral_variance(int64_t batch, int32_t n, const void* s, float weight,
                                    const float* weights, double* loss, void* grad, int32_t accumulate,
-                                   void* stream) {
+                                   int32_t ddof, void* stream) {
   t_launches = 0;
   if (batch < 1 || batch > (1LL << 31) - 1) return fail(GRAF_EINVAL, "batch = %lld", (long long)batch);
   if (!is_pow2(n) || n < 2) return fail(GRAF_EINVAL, "N = %d is not a power of two >= 2", n);
   if (n > GRAF_MAX_M) return fail(GRAF_EUNSUPPORTED, "N = %d > %d", n, GRAF_MAX_M);
   if (!s || !grad || !aligned8(s) || !aligned8(grad)) return fail(GRAF_EINVAL, "s / grad NULL or misaligned");
   if (!std::isfinite(weight)) return fail(GRAF_EINVAL, "non-finite weight");
-  cudaError_t e = ensure_twiddles();
-  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
+  if (ddof != 0 && ddof != 1) return fail(GRAF_EINVAL, "ddof must be 0 or 1");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaError_t e = ensure_twiddles(cs);
+  if (e != cudaSuccess) return cuda_fail(e, "twiddle table init");
   SvParams q{static_cast<const float2*>(s), n, weight, weights, accumulate ? 1 : 0, loss,
-             static_cast<float2*>(grad)};
+             static_cast<float2*>(grad), (int)ddof};
   if (n <= 32) {
     const int threads = 32;
     const size_t smem = sizeof(float2) * 2 * (size_t)n + sizeof(double) * threads;

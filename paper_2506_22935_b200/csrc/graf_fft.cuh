@@ -31,11 +31,24 @@ namespace graf {
 
 constexpr int kMaxM = 16384;
 
-// M-th roots of unity table, g_tw[i] = exp(-2 pi i * i / kMaxM), float32
-// correctly rounded from extended precision on the host (graf_api.cu).  Each
-// translation unit of the library (graf_api.cu, graf_rows_*.cu) holds its own
-// copy; ensure_twiddles() uploads all of them.
+// M-th roots of unity table, g_tw[i] = exp(-2 pi i * i / kMaxM), float32, rounded
+// once from double sincospi (exact at multiples of 1/4 turn).  Each translation unit
+// of the library (graf_api.cu, graf_rows_*.cu) holds its own copy and fills it with
+// its own tw_init_kernel; ensure_twiddles() (graf_api.cu) enqueues all of them on the
+// caller's stream (no host-blocking copy).
 static __device__ float2 g_tw[kMaxM];
+
+static __global__ void tw_init_kernel() {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < kMaxM; j += gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincospi(-2.0 * (double)j / (double)kMaxM, &sn, &cs);
+    g_tw[j] = make_float2((float)cs, (float)sn);
+  }
+}
+static inline cudaError_t launch_tw_init(cudaStream_t st) {
+  tw_init_kernel<<<kMaxM / 256, 256, 0, st>>>();
+  return cudaGetLastError();
+}
 
 // Complex add / subtract.  sm_100 has paired fp32 instructions (FADD2 / FMUL2 /
 // FFMA2: one issue slot for the real and imaginary lanes); GRAF_F32X2 selects them

@@ -81,6 +81,9 @@ struct RowParams {
   // single pass is valid (guard[b].reserved == 1).
   int onepass;
   const graf_partials* guard;
+  // caller's per-waveform skip mask (graf_af_desc.skip, ABI v6): skip[b] != 0 -> no work,
+  // no output for waveform b
+  const int32_t* skip;
   // cross-ambiguity (CROSS kernels): X = sum s[n] conj(s2[n-k]) W^{mn}; rows unfolded
   const float2* s2;    // [B][N]
   float2* gpart2;      // [B][P][N] partial dL/ds2*
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float2* sg = p.s + (size_t)b * N;
   if (p.guard && p.guard[b].reserved == 1.0) return;   // fallback launch: this waveform is done
+  if (p.skip && p.skip[b]) return;                       // the caller skips this waveform
 
   // ---- shared-memory carve-up: [scratch 64 doubles][s_pad N+M][exchange x S][g x S]
   // s_pad holds s[n] for n in [-N, M): N zeros, the N samples, M-N zeros, so the
@@ -1301,6 +1305,7 @@ struct ReduceParams {
   graf_partials* out;
   int onepass;   // records of the single pass: reserved = 1 where it is valid (R13 rule)
   float xbar;
+  const int32_t* skip;   // skipped waveforms get identity partials (no stale records)
 };
 
 // one warp per waveform: lane l merges records l, l+32, ... in order, then a fixed
@@ -1319,7 +1324,8 @@ __global__ void partials_reduce_kernel(ReduceParams r) {
   if (b >= r.B) return;   // warp-uniform
   double S = 0, Z = 0, Cs = 0, key = (double)0x7fffffff;
   double m = -INFINITY;
-  for (int q = lane; q < r.P; q += 32) {
+  const int P = (r.skip && r.skip[b]) ? 0 : r.P;
+  for (int q = lane; q < P; q += 32) {
     const double* rec = r.part + ((size_t)b * r.P + q) * kPart;
     merge_rec(S, m, Z, Cs, key, rec[0], rec[1], rec[2], rec[3], rec[5], r.T);
   }
@@ -1368,10 +1374,12 @@ struct FinalizeParams {
   // delay-sharded single pass (graf_af_loss_grad_sp_end): the ISL sum comes from `global`,
   // and a waveform whose global single pass is invalid gets loss NaN and grad 0
   int sp;
+  const int32_t* skip;   // skipped waveforms: outputs left untouched
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   const int b = blockIdx.x;
+  if (f.skip && f.skip[b]) return;
   const int N = f.N;
   const float2* sg = f.s + (size_t)b * N;
   const float2* sg2 = f.s2 ? f.s2 + (size_t)b * N : nullptr;
@@ -1451,6 +1459,18 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
       const float2 s2v = sg2[n];
       f.grad2[(size_t)b * N + n] = make_float2((float)hx - coef2 * s2v.x, (float)hy - coef2 * s2v.y);
     }
+  }
+}
+
+// A shard that owns no loss rows: grad = 0 (and loss = 0 for losses that are sums over
+// rows), skipped waveforms untouched.
+__global__ void zero_outputs_kernel(float2* grad, double* loss, long long B, int N, const int32_t* skip) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < B * N;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / N;
+    if (skip && skip[b]) continue;
+    grad[i] = make_float2(0.f, 0.f);
+    if (loss && i - b * N == 0) loss[b] = 0.0;
   }
 }
 
@@ -1567,10 +1587,12 @@ struct PslParams {
   int accumulate;     // 1: add into loss/grad (a finalize wrote them), 0: overwrite
   double* loss;       // nullable
   float2* grad;
+  const int32_t* skip;
 };
 
 __global__ void __launch_bounds__(256) psl_grad_kernel(PslParams q) {
   const int b = blockIdx.x;
+  if (q.skip && q.skip[b]) return;
   const int N = q.N, M = q.M;
   const float2* sg = q.s + (size_t)b * N;
   const graf_partials st = q.stats[b];
@@ -1641,8 +1663,8 @@ __global__ void __launch_bounds__(256) psl_grad_kernel(PslParams q) {
 
 // ---------------------------------------------------------------------------
 // Spectral variance (the section-7 LPI term; reading R22):
-//   S = DFT_N(s), p = |S|^2 / P, SV = sum (p - mean p)^2 / (N - 1)
-//   dSV/dS* = (c - sum c p) S / P, c = 2 (p - mean p) / (N - 1);  g = DFT^H (dSV/dS*)
+//   S = DFT_N(s), p = |S|^2 / P, SV = sum (p - mean p)^2 / (N - ddof)
+//   dSV/dS* = (c - sum c p) S / P, c = 2 (p - mean p) / (N - ddof);  g = DFT^H (dSV/dS*)
 // N <= 1024: the DFT as its sum (one CTA per waveform, a thread per bin; the
 // section-7 N = 256 costs microseconds); N >= 2048: the Stockham row FFT.
 // Reductions: fixed-order shared-memory trees (deterministic).
@@ -1655,6 +1677,7 @@ struct SvParams {
   int accumulate;
   double* loss;
   float2* grad;
+  int ddof;               // variance denominator N - ddof (0: population; 1: unbiased)
 };
 
 // sum over the CTA (blockDim.x a power of two <= 1024), result in every thread
@@ -1706,10 +1729,10 @@ __global__ void __launch_bounds__(1024) sv_direct_kernel(SvParams q) {
   const double mean = cta_tree_sum(t < N ? pe : 0.0, buf) / N;
   const double d = pe - mean;
   const double var = cta_tree_sum(t < N ? d * d : 0.0, buf);
-  const double ce = 2.0 * d / (N - 1);
+  const double ce = 2.0 * d / (N - q.ddof);
   const double cp = cta_tree_sum(t < N ? ce * pe : 0.0, buf);
   const float wb = q.weights ? q.weights[b] : q.weight;
-  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)wb * (var / (N - 1));
+  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)wb * (var / (N - q.ddof));
   if (t < N) {
     const double f = (double)wb * (ce - cp) / P;
     ds[t] = make_float2((float)(f * Sx), (float)(f * Sy));
@@ -1778,14 +1801,14 @@ __global__ void __launch_bounds__(M / E) sv_fft_kernel(SvParams q) {
     const double pe = ((double)v[e].x * v[e].x + (double)v[e].y * v[e].y) / P;
     const double d = pe - mean;
     var += d * d;
-    const double ce = 2.0 * d / (M - 1);
+    const double ce = 2.0 * d / (M - q.ddof);
     c[e] = (float)ce;
     cp += ce * pe;
   }
   var = cta_tree_sum(var, buf);
   cp = cta_tree_sum(cp, buf);
   const float wb = q.weights ? q.weights[b] : q.weight;
-  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)wb * (var / (M - 1));
+  if (t == 0 && q.loss) q.loss[b] = (q.accumulate ? q.loss[b] : 0.0) + (double)wb * (var / (M - q.ddof));
   const float sc = (float)((double)wb / P);
   const float cpf = (float)cp;
 #pragma unroll

@@ -5,7 +5,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -16,7 +15,20 @@ namespace graf {
 
 extern thread_local int t_launches;   // kernels / memsets enqueued by the current entry-point call
 constexpr int kMaxDev = 64;
-constexpr int kNumSM = 148;  // B200; the plan is a pure function of the descriptors
+
+// SM count of the current device (cached per device; the workspace bound and the
+// launch plan use the same value for the same device)
+inline int device_sm_count() {
+  static int cache[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
 
 // ---------------------------------------------------------------------------
 // launch plan
@@ -91,7 +103,7 @@ cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
 
 template <int M, int KIND, bool WGT, bool CROSS = false>
 cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
-  int occ = 1, nsm = kNumSM;
+  int occ = 1, nsm = device_sm_count();
   // (also sets the instantiation's large-shared-memory attribute, once per device)
   cudaError_t e0 = kernel_occupancy<M, KIND, WGT, CROSS>(pl.smem, &occ, &nsm);
   if (e0 != cudaSuccess) return e0;
@@ -136,12 +148,9 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   }
   if (!pl.fixedP) {
     pl.P = choose_P(pl, B, occ, nsm);
-    // tuning knob (scripts/c2_rows.py): GRAF_FORCE_P=<P> overrides the model's choice
-    static const int kForceP = [] {
-      const char* v = std::getenv("GRAF_FORCE_P");
-      return v ? std::atoi(v) : 0;
-    }();
-    if (kForceP > 0) pl.P = std::min(kForceP, std::max(pl.Pbound, 1));
+#ifdef GRAF_FORCE_P   // tuning builds only (scripts/c2_rows.py): -DGRAF_FORCE_P=<P> overrides the model
+    pl.P = std::min(GRAF_FORCE_P, std::max(pl.Pbound, 1));
+#endif
     pl.fixedP = true;   // later passes of the same call reuse it
   }
   rp.fuse = 0;
@@ -214,8 +223,8 @@ cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st,
 // one instantiation per size, defined in graf_rows_*.cu
 template <int M>
 cudaError_t launch_rows_size(Plan& pl, const RowParams& rp, int B, cudaStream_t st, int kind);
-// upload of the twiddle table into one translation unit's copy
-using TwUpload = cudaError_t (*)(const float2*);
-std::vector<TwUpload>& tw_uploaders();
+// fill of one translation unit's copy of the twiddle table, enqueued on a stream
+using TwFill = cudaError_t (*)(cudaStream_t);
+std::vector<TwFill>& tw_fillers();
 
 }  // namespace graf

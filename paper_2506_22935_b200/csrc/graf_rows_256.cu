@@ -3,9 +3,10 @@
 
 namespace graf {
 namespace {
-cudaError_t upload(const float2* h) { return cudaMemcpyToSymbol(g_tw, h, sizeof(float2) * kMaxM); }
+// this unit's copy of the twiddle table, filled on the caller's stream
+cudaError_t tw_fill(cudaStream_t st) { return launch_tw_init(st); }
 struct Register {
-  Register() { tw_uploaders().push_back(&upload); }
+  Register() { tw_fillers().push_back(&tw_fill); }
 } register_tw;
 }  // namespace
 

@@ -80,8 +80,16 @@ def _check_s(s: torch.Tensor) -> torch.Tensor:
     return s.contiguous()
 
 
+def _skip_ptr(skip: Optional[torch.Tensor], B: int):
+    if skip is None:
+        return None
+    if skip.dtype != torch.int32 or not skip.is_cuda or skip.shape != (B,) or not skip.is_contiguous():
+        raise ValueError("graf: skip must be a contiguous int32 CUDA tensor of shape [B]")
+    return ctypes.c_void_p(skip.data_ptr())
+
+
 def _desc(s: torch.Tensor, M: int, out=None, layout="centered", k_begin=None, k_end=None,
-          normalize_output=False, shard=(0, 1), periodic=False) -> L.AfDesc:
+          normalize_output=False, shard=(0, 1), periodic=False, skip=None) -> L.AfDesc:
     B, N = s.shape
     if periodic:   # Alg. 1: delays 0..N-1 (mod N)
         kb = 0 if k_begin is None else int(k_begin)
@@ -89,7 +97,8 @@ def _desc(s: torch.Tensor, M: int, out=None, layout="centered", k_begin=None, k_
         kb = -(N - 1) if k_begin is None else int(k_begin)
     ke = N if k_end is None else int(k_end)
     return L.AfDesc(L.ABI_VERSION, int(N), int(M), _OUT[out], int(B), kb, ke, _LAYOUT[layout],
-                    int(bool(normalize_output)), int(shard[0]), int(shard[1]), int(bool(periodic)))
+                    int(bool(normalize_output)), int(shard[0]), int(shard[1]), int(bool(periodic)),
+                    _skip_ptr(skip, B))
 
 
 def workspace_bytes(desc: L.AfDesc, loss: Optional[L.LossDesc]) -> int:
@@ -123,15 +132,18 @@ def _surface_alloc(desc: L.AfDesc, device) -> Optional[torch.Tensor]:
 def af_forward(s: torch.Tensor, M: int, *, out: Optional[str] = "c64", layout: str = "centered",
                k_begin: Optional[int] = None, k_end: Optional[int] = None, normalize_output: bool = False,
                loss: Optional[LossSpec] = None, shard=(0, 1), ws: Optional[Workspace] = None,
-               surface: Optional[torch.Tensor] = None, stream=None, periodic: bool = False):
+               surface: Optional[torch.Tensor] = None, stream=None, periodic: bool = False,
+               skip: Optional[torch.Tensor] = None, partials: Optional[torch.Tensor] = None):
     """graf_af_forward: surface window and/or this shard's loss partials [B,6] (float64).
-    periodic=True: the paper's circular surface (Eq. 2 / Alg. 1), M == N."""
+    periodic=True: the paper's circular surface (Eq. 2 / Alg. 1), M == N.
+    skip: int32 [B] device mask, waveforms with skip[b] != 0 are left untouched (ABI v6)."""
     s = _check_s(s)
-    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic)
+    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic, skip)
     ld = loss.desc() if loss is not None else None
     if surface is None:
         surface = _surface_alloc(d, s.device)
-    partials = torch.empty((s.shape[0], NPART), dtype=torch.float64, device=s.device) if loss is not None else None
+    if partials is None and loss is not None:
+        partials = torch.empty((s.shape[0], NPART), dtype=torch.float64, device=s.device)
     nbytes = workspace_bytes(d, ld)
     wp, wn = (ws or _ws).get(nbytes, s.device)
     L.check(L.lib().graf_af_forward(ctypes.byref(d), ctypes.byref(ld) if ld else None,
@@ -145,10 +157,12 @@ def af_loss_grad(s: torch.Tensor, M: int, loss: LossSpec, *, global_partials: Op
                  normalize_output: bool = False, shard=(0, 1), ws: Optional[Workspace] = None,
                  grad: Optional[torch.Tensor] = None, loss_out: Optional[torch.Tensor] = None,
                  surface: Optional[torch.Tensor] = None, want_loss: bool = True, stream=None,
-                 periodic: bool = False):
-    """graf_af_loss_grad -> (loss[B] float64, grad[B,N] complex64 = dL/ds*, surface or None)."""
+                 periodic: bool = False, skip: Optional[torch.Tensor] = None):
+    """graf_af_loss_grad -> (loss[B] float64, grad[B,N] complex64 = dL/ds*, surface or None).
+    skip: int32 [B] device mask; the outputs of waveforms with skip[b] != 0 (in the given
+    loss_out / grad buffers) are left untouched (ABI v6)."""
     s = _check_s(s)
-    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic)
+    d = _desc(s, M, out, layout, k_begin, k_end, normalize_output, shard, periodic, skip)
     ld = loss.desc()
     B, N = s.shape
     if grad is None:
@@ -306,8 +320,9 @@ def af_loss(s, M, spec: LossSpec, periodic=False):
 # ---------------------------------------------------------------------------
 def spectral_variance(s: torch.Tensor, weight: float = 1.0, weights: Optional[torch.Tensor] = None,
                       loss: Optional[torch.Tensor] = None, grad: Optional[torch.Tensor] = None,
-                      accumulate: bool = False, stream=None):
-    """graf_spectral_variance -> (weight*SV [B] float64, weight*dSV/ds* [B,N] complex64)."""
+                      accumulate: bool = False, ddof: int = 0, stream=None):
+    """graf_spectral_variance -> (weight*SV [B] float64, weight*dSV/ds* [B,N] complex64);
+    ddof = 0 population variance, 1 unbiased."""
     s = _check_s(s)
     B, N = s.shape
     if loss is None:
@@ -318,7 +333,7 @@ def spectral_variance(s: torch.Tensor, weight: float = 1.0, weights: Optional[to
         assert weights.dtype == torch.float32 and weights.is_cuda and weights.shape == (B,)
     L.check(L.lib().graf_spectral_variance(B, N, ctypes.c_void_p(s.data_ptr()), float(weight), _ptr(weights),
                                            _ptr(loss), ctypes.c_void_p(grad.data_ptr()), int(bool(accumulate)),
-                                           _stream(stream)))
+                                           int(ddof), _stream(stream)))
     return loss, grad
 
 

@@ -15,14 +15,15 @@ One process per GPU.  Two partitionings of the same hot path:
        already includes the shard's share of the normalisation term (linear in
        its own partial sums), so the sum is the full dL/ds*.
   ISL-only losses are linear in the per-row sums, so step 1 is skipped and the
-  per-shard losses are summed with the gradient.
+  per-shard losses are summed with the gradient.  Hard PSL (lambda_hpsl) needs the
+  global max, so it runs step 1 like soft-PSL.
   The full-plane normalised soft-PSL (c5) runs ONE pass per shard instead of two
   (reading R13 across shards, R27).  Phase 1 computes each shard's partials, including
   the centred sum sum expm1((x - xbar)/T); those are all-gathered and combined.  Phase 2
   scales each shard's gradient by the global 1/Z_c, and then comes the gradient
-  all_reduce.  If the global validity rule fails for any waveform, every rank falls back
-  to the two-pass protocol for the batch; all ranks hold the same combined partials, so
-  they all decide the same way.
+  all_reduce.  Waveforms outside the global validity rule are recomputed by the two-pass
+  protocol with the others masked out (graf_af_desc.skip): the decision stays on the
+  device, so there is no host synchronisation and the step is graph-capturable.
 
 `backend` is the object that runs the per-shard compute; the default calls the
 C ABI (graf_af_forward / graf_af_loss_grad / graf_combine_partials).  Tests on CPU
@@ -42,13 +43,19 @@ __all__ = ["GrafBackend", "batch_slice", "batch_sharded_loss_grad", "delay_shard
 
 
 class GrafBackend:
-    """Per-shard compute through the C ABI (device tensors)."""
+    """Per-shard compute through the C ABI (device tensors).  Each instance owns its
+    workspaces (the single pass keeps its unscaled gradient in `ws_sp` between phases)."""
 
-    def forward_partials(self, s, M, spec, shard):
-        return _graf.af_forward(s, M, out=None, loss=spec, shard=shard)[1]
+    def __init__(self):
+        self.ws = _graf.Workspace()
+        self.ws_sp = _graf.Workspace()
 
-    def loss_grad(self, s, M, spec, global_partials, shard):
-        loss, g, _ = _graf.af_loss_grad(s, M, spec, global_partials=global_partials, shard=shard)
+    def forward_partials(self, s, M, spec, shard, skip=None):
+        return _graf.af_forward(s, M, out=None, loss=spec, shard=shard, ws=self.ws, skip=skip)[1]
+
+    def loss_grad(self, s, M, spec, global_partials, shard, skip=None, loss_out=None, grad=None):
+        loss, g, _ = _graf.af_loss_grad(s, M, spec, global_partials=global_partials, shard=shard, ws=self.ws,
+                                        skip=skip, loss_out=loss_out, grad=grad)
         return loss, g
 
     def combine(self, spec, parts):
@@ -57,15 +64,11 @@ class GrafBackend:
     def single_pass_eligible(self, s, M, spec, shard):
         return _graf.single_pass_eligible(s, M, spec, shard)
 
-    _sp_ws = None   # the single pass keeps its unscaled gradient here between the phases
-
     def sp_begin(self, s, M, spec, shard):
-        if GrafBackend._sp_ws is None:
-            GrafBackend._sp_ws = _graf.Workspace()
-        return _graf.af_loss_grad_sp_begin(s, M, spec, shard, ws=GrafBackend._sp_ws)
+        return _graf.af_loss_grad_sp_begin(s, M, spec, shard, ws=self.ws_sp)
 
     def sp_end(self, s, M, spec, glob, shard):
-        return _graf.af_loss_grad_sp_end(s, M, spec, shard, glob, ws=GrafBackend._sp_ws)
+        return _graf.af_loss_grad_sp_end(s, M, spec, shard, glob, ws=self.ws_sp)
 
 
 def _world(group) -> Tuple[int, int]:
@@ -85,47 +88,68 @@ def batch_sharded_loss_grad(s_all: torch.Tensor, M: int, spec, group=None, backe
                             gather_loss: bool = False):
     """Batch sharding: this rank's waveforms only; no data-path collective.
     Returns (slice, loss[b], grad[b]) for the local block; with gather_loss the
-    full loss vector is all-gathered for reporting (off the hot path)."""
+    full loss vector [B] is all-gathered for reporting (off the hot path)."""
     backend = backend or GrafBackend()
     r, G = _world(group)
-    sl = batch_slice(s_all.shape[0], r, G)
+    B = s_all.shape[0]
+    sl = batch_slice(B, r, G)
     loss, g = backend.loss_grad(s_all[sl], M, spec, None, (0, 1))
     if gather_loss and G > 1:
-        parts = [torch.empty_like(loss) for _ in range(G)]
-        dist.all_gather(parts, loss, group=group)   # equal blocks assumed for reporting
-        loss = torch.cat(parts)
+        # blocks differ in size by at most one: pad every block to ceil(B/G) so the
+        # collective moves equal-size buffers, then trim by the known slices
+        bmax = -(-B // G)
+        pad = torch.zeros((bmax,), dtype=loss.dtype, device=loss.device)
+        pad[:loss.shape[0]] = loss
+        parts = [torch.empty_like(pad) for _ in range(G)]
+        dist.all_gather(parts, pad, group=group)
+        loss = torch.cat([parts[q][:batch_slice(B, q, G).stop - batch_slice(B, q, G).start] for q in range(G)])
     return sl, loss, g
+
+
+def _gather_combine(backend, spec, part, G, group):
+    gathered = [torch.empty_like(part) for _ in range(G)]
+    dist.all_gather(gathered, part.contiguous(), group=group)
+    return backend.combine(spec, torch.stack(gathered))
 
 
 def delay_sharded_loss_grad(s: torch.Tensor, M: int, spec, group=None, backend=None):
     """Delay sharding of every waveform in `s` across the ranks of `group`.
-    Returns (loss[B] float64, grad[B, N] complex64 = dL/ds*), identical on all ranks."""
+    Returns (loss[B] float64, grad[B, N] complex64 = dL/ds*), identical on all ranks.
+    No host synchronisation on any branch (the single pass's fallback decision stays on
+    the device), so a step can be captured in a CUDA graph with its NCCL collectives."""
     backend = backend or GrafBackend()
     r, G = _world(group)
     shard = (r, G)
     if G == 1:
         return backend.loss_grad(s, M, spec, None, (0, 1))
-    if spec.lambda_psl == 0:
-        # ISL-only: one fused pass per shard; loss and gradient are sums over shards
+    hpsl = getattr(spec, "lambda_hpsl", 0.0) != 0
+    match = getattr(spec, "lambda_match", 0.0) != 0
+    if spec.lambda_psl == 0 and not hpsl:
+        # ISL / match only: linear in the rows, one fused pass per shard; loss and gradient
+        # are sums over shards
         loss, g = backend.loss_grad(s, M, spec, None, shard)
         dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
         return loss, g
+    if match:
+        raise NotImplementedError("delay sharding of a match loss with soft/hard PSL: the match term "
+                                  "needs unsharded calls in v1 (graf_af_loss_grad rejects it with `global`)")
     if hasattr(backend, "sp_begin") and backend.single_pass_eligible(s, M, spec, shard):
         # full-plane soft-PSL: one pass per shard, the global 1/Z_c applied in phase 2
-        part = backend.sp_begin(s, M, spec, shard)
-        gathered = [torch.empty_like(part) for _ in range(G)]
-        dist.all_gather(gathered, part.contiguous(), group=group)
-        glob = backend.combine(spec, torch.stack(gathered))
+        glob = _gather_combine(backend, spec, backend.sp_begin(s, M, spec, shard), G, group)
         loss, g, valid = backend.sp_end(s, M, spec, glob, shard)
-        if bool(valid.all()):      # identical on every rank (same combined partials)
-            dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
-            return loss, g
-    # soft-PSL: pass 1 partials -> all_gather -> combine (rank order) -> pass 2 -> all_reduce
-    part = backend.forward_partials(s, M, spec, shard)
-    gathered = [torch.empty_like(part) for _ in range(G)]
-    dist.all_gather(gathered, part.contiguous(), group=group)
-    glob = backend.combine(spec, torch.stack(gathered))
+        # device-side fallback: the two-pass protocol over the waveforms whose single pass
+        # broke the R13 rule (valid == 0); valid waveforms are skipped (their CTAs exit at
+        # once, their loss / grad are left as phase 2 wrote them).  Every rank holds the
+        # same `valid`, so the collectives below match.
+        skip = valid.to(torch.int32).contiguous()
+        glob2 = _gather_combine(backend, spec, backend.forward_partials(s, M, spec, shard, skip=skip), G, group)
+        loss, g = backend.loss_grad(s, M, spec, glob2, shard, skip=skip, loss_out=loss, grad=g)
+        dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
+        return loss, g
+    # soft-PSL / hard PSL: pass 1 partials -> all_gather -> combine (rank order) -> pass 2
+    # (hard PSL: the global argmax key travels in the partials) -> all_reduce of g
+    glob = _gather_combine(backend, spec, backend.forward_partials(s, M, spec, shard), G, group)
     loss, g = backend.loss_grad(s, M, spec, glob, shard)
     dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
     return loss, g

@@ -1,0 +1,54 @@
+#!/usr/bin/env python
+"""Write the c5 oracle golden (tests/golden/c5_w0_softpsl.npz) — calls only oracle/.
+
+Config 5 (BASELINE.json configs[4]): N = M = 16384, random phase, full-plane
+normalised ISL + log-sum-exp soft-PSL (T = 0.01).  The float64 oracle
+(oracle/graf_oracle.py, loss_and_grad_chunked: every A[k,m] is the direct sum,
+SURVEY.md §8(c) steps 1-8) is run on waveform 0 with lambda_isl = 0, lambda_psl = 1.
+
+Why lambda_isl = 0: on the full plane the normalised ISL is the constant M - 1 with an
+identically zero gradient (volume identity; pinned by
+tests/test_oracle_pins.py), so the c5 gradient IS the soft-PSL gradient.  The soft-PSL
+gradient at N = 16384 is ~1e-11 while the ISL terms it would be summed with are O(1):
+in float64 those O(1) terms leave ~1e-16-relative rounding residue, which the
+lambda_isl = 0 run avoids.  The ISL value (S/E^2) is computed in the same sweep and
+stored, so the c5 loss is isl + lse.
+
+Cost: three 32767 x 16384 x 16384 complex matrix products (~2.1e14 flops); ~25-40 min
+on 8 cores.  Run once:  python scripts/make_c5_golden.py
+"""
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from graf_inputs import CONFIGS, config_waveforms  # noqa: E402
+from oracle import graf_oracle as O  # noqa: E402
+
+
+def main():
+    cfg = CONFIGS[5]
+    N, M = cfg["N"], cfg["M"]
+    s = config_waveforms(5, batch=1)[0]
+    spec = O.LossSpec.from_dict(dict(cfg["loss"], lambda_isl=0.0, lambda_psl=1.0))
+    t0 = time.time()
+    L, g, t = O.loss_and_grad_chunked(s, M, spec, chunk_rows=512, chunk_bins=M)
+    el = time.time() - t0
+    out = os.path.join(ROOT, "tests", "golden", "c5_w0_softpsl.npz")
+    np.savez_compressed(
+        out, s_sha256=np.array(hashlib.sha256(np.ascontiguousarray(s).tobytes()).hexdigest()),
+        N=N, M=M, temperature=spec.temperature, lse=t["lse"], isl=t["isl"], S=t["S"], c=t["c"], Z=t["Z"],
+        E=t["E"], count=t["count"], sigma_g=t["sigma_g"], loss_softpsl=L, loss_c5=t["isl"] + t["lse"],
+        grad=g.astype(np.complex128), seconds=el,
+        note=np.array("oracle/graf_oracle.py loss_and_grad_chunked, waveform 0 of config 5, "
+                      "lambda_isl=0 lambda_psl=1 T=0.01 full plane minus origin, normalised"))
+    print(f"wrote {out} in {el:.0f} s: lse={t['lse']!r} isl={t['isl']!r} max|g|={np.abs(g).max():.3e}")
+
+
+if __name__ == "__main__":
+    main()

@@ -84,7 +84,7 @@ def test_surface_large_sampled_rows(N, M):
         assert np.abs(surf.cpu().numpy()[0] - ref).max() <= 1e-5 * E, k
 
 
-def test_c3_surface_families_and_lfm_closed_form():
+def test_c3_surface_families_vs_oracle_subset():
     cfg = CONFIGS[3]
     s = config_waveforms(3, batch=6)
     surf, _ = graf.af_forward(dev(s), cfg["M"], out="abs", layout="centered")

@@ -90,20 +90,22 @@ def test_hard_psl_sharding_algebra():
         assert (gsum - g1).abs().max().item() <= 1e-4 * g1.abs().max().item()
 
 
+@pytest.mark.parametrize("ddof", [0, 1])
 @pytest.mark.parametrize("N", [2, 8, 32, 64, 128, 256, 512, 1024, 2048, 4096])
-def test_spectral_variance(N):
+def test_spectral_variance(N, ddof):
     s = cg(3, N, N + 1)
     w = torch.tensor([1.0, 0.5, 3.0], dtype=torch.float32, device="cuda")
-    loss, g = graf.spectral_variance(dev(s), weights=w)
+    loss, g = graf.spectral_variance(dev(s), weights=w, ddof=ddof)
     for b in range(3):
-        sv, gref = O.spectral_variance_and_grad(s[b])
+        sv, gref = O.spectral_variance_and_grad(s[b], ddof=ddof)
         wb = float(w[b])
         assert abs(loss[b].item() - wb * sv) <= 1e-4 * wb * sv + 1e-12
         assert np.abs(g[b].cpu().numpy() - wb * gref).max() <= 1e-4 * wb * np.abs(gref).max() + 1e-12
     # accumulate mode adds onto an existing loss / gradient
     l0 = torch.ones(3, dtype=torch.float64, device="cuda")
     g0 = torch.ones((3, N), dtype=torch.complex64, device="cuda")
-    l1, g1 = graf.spectral_variance(dev(s), weights=w, loss=l0.clone(), grad=g0.clone(), accumulate=True)
+    l1, g1 = graf.spectral_variance(dev(s), weights=w, loss=l0.clone(), grad=g0.clone(), accumulate=True,
+                                    ddof=ddof)
     assert torch.allclose(l1 - 1.0, loss, rtol=1e-9, atol=1e-15)
     assert (g1 - 1.0 - g).abs().max().item() <= 1e-6 * max(1.0, g.abs().max().item())
 
@@ -117,7 +119,9 @@ def test_spectral_variance_large_invariants():
     assert ip.abs().max().item() <= 1e-4 * (g.abs() * s.abs()).sum(dim=1).max().item()
     tone = torch.exp(2j * np.pi * 7 * torch.arange(N, dtype=torch.float64) / N).to(torch.complex64).cuda()[None]
     lt, _ = graf.spectral_variance(tone)
-    assert abs(lt.item() - 1.0 / N) <= 1e-3 / N
+    assert abs(lt.item() - (N - 1) / N ** 2) <= 1e-3 / N          # population variance
+    ones = torch.ones((1, 4), dtype=torch.complex64, device="cuda")
+    assert abs(graf.spectral_variance(ones)[0].item() - 0.1875) <= 1e-6   # SPEC.md L331 example
 
 
 def test_phase_adam_matches_oracle():

@@ -476,19 +476,23 @@ def test_spectral_variance_closed_forms_and_gradient():
     d = np.zeros(n, complex); d[3] = 1.0
     sv, g = O.spectral_variance_and_grad(d)
     assert abs(sv) < 1e-30 and np.abs(g).max() < 1e-15
-    # single tone: all power in one bin -> p = e_j, var = ((1 - 1/N)^2 + (N-1)/N^2)/(N-1) = 1/N
+    # single tone: all power in one bin -> p = e_j, sum (p - 1/N)^2 = (N-1)/N, so the
+    # population variance is (N-1)/N^2 and the unbiased one 1/N
     tone = np.exp(2j * np.pi * 5 * np.arange(n) / n)
-    sv, _ = O.spectral_variance_and_grad(tone)
-    assert abs(sv - 1.0 / n) < 1e-14
-    # matches numpy.fft + an unbiased variance on random input; central differences
+    assert abs(O.spectral_variance_and_grad(tone)[0] - (n - 1) / n ** 2) < 1e-15
+    assert abs(O.spectral_variance_and_grad(tone, ddof=1)[0] - 1.0 / n) < 1e-14
+    # SPEC.md L331 worked example: all-ones N = 4 -> p = [1,0,0,0] -> 3/16 (population)
+    assert abs(O.spectral_variance_and_grad(np.ones(4, complex))[0] - 0.1875) < 1e-16
+    # matches numpy.fft + numpy's variance (both ddof) on random input; central differences
     s = rs(n, 96)
     S = np.fft.fft(s)
     p = np.abs(S) ** 2 / np.sum(np.abs(S) ** 2)
-    sv, g = O.spectral_variance_and_grad(s)
-    assert abs(sv - np.var(p, ddof=1)) < 1e-15
-    fd = _fd(lambda z: O.spectral_variance_and_grad(z)[0], s)
-    np.testing.assert_allclose(2 * g, fd, atol=1e-7 * np.abs(fd).max())
-    assert abs(np.vdot(g, s)) < 1e-12                           # scale- and phase-invariant
+    for ddof in (0, 1):
+        sv, g = O.spectral_variance_and_grad(s, ddof=ddof)
+        assert abs(sv - np.var(p, ddof=ddof)) < 1e-15
+        fd = _fd(lambda z: O.spectral_variance_and_grad(z, ddof=ddof)[0], s)
+        np.testing.assert_allclose(2 * g, fd, atol=1e-7 * np.abs(fd).max())
+        assert abs(np.vdot(g, s)) < 1e-12                       # scale- and phase-invariant
 
 
 def test_adam_matches_torch_and_first_step():

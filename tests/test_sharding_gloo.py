@@ -36,33 +36,49 @@ class OracleShardBackend:
         A = O.ambiguity(s, self.M, rows_all[keep], bins)
         return rows_all[keep], bins, mask[keep], w[keep], A
 
-    def forward_partials(self, s_b, M, spec, shard):
+    def _key_lo(self, spec):
+        return -min(spec.k_max, self.N - 1)
+
+    def forward_partials(self, s_b, M, spec, shard, skip=None):
         out = []
-        for s in s_b.numpy():
+        for b, s in enumerate(s_b.numpy()):
+            if skip is not None and int(skip[b]):
+                out.append([0.0, -np.inf, 0.0, 0.0, float(0x7fffffff), 0.0])   # identity partials
+                continue
             rows, bins, mask, w, A = self._cells(s, spec, shard)
             E = O.energy(s)
             chi = np.abs(A) ** 2
             x = chi / E ** 2 if spec.normalize else chi
             S = float(np.sum(w[mask] * chi[mask]))
+            key = float(0x7fffffff)
             if mask.any():
                 c = float(np.max(x[mask]))
                 Z = float(np.sum(np.exp((x[mask] - c) / spec.temperature)))
+                # hard PSL: row-major key (delay index from key_lo) * M + raw bin of the
+                # lowest-keyed maximal cell (include/graf.h graf_partials.psl_key)
+                ii, jj = np.nonzero(mask & (x == c))
+                key = float(min((int(rows[i]) - self._key_lo(spec)) * M + int(bins[j]) for i, j in zip(ii, jj)))
             else:
                 c, Z = -np.inf, 0.0
-            out.append([S, c, Z, 0.0, 0.0, 0.0])
+            out.append([S, c, Z, 0.0, key, 0.0])
         return torch.tensor(out, dtype=torch.float64)
 
     def combine(self, spec, parts):
         from paper_2506_22935_b200 import graf
         return graf.combine_partials(spec, parts)
 
-    def loss_grad(self, s_b, M, spec, glob, shard):
-        if glob is None and spec.lambda_psl != 0:
+    def loss_grad(self, s_b, M, spec, glob, shard, skip=None, loss_out=None, grad=None):
+        hpsl = getattr(spec, "lambda_hpsl", 0.0)
+        if glob is None and (spec.lambda_psl != 0 or hpsl != 0):
             # like graf_af_loss_grad with global = NULL: this call's own partials
             glob = self.forward_partials(s_b, M, spec, shard)
         losses, grads = [], []
         T = spec.temperature
         for b, s in enumerate(s_b.numpy()):
+            if skip is not None and int(skip[b]):
+                losses.append(loss_out[b].item())
+                grads.append(grad[b].numpy())
+                continue
             rows, bins, mask, w, A = self._cells(s, spec, shard)
             E = O.energy(s)
             chi = np.abs(A) ** 2
@@ -73,14 +89,32 @@ class OracleShardBackend:
                 S, c, Z = float(np.sum(w[mask] * chi[mask])), 0.0, 1.0
             lse = c + T * np.log(Z)
             isl = S / E ** 2 if spec.normalize else S
-            losses.append(spec.lambda_isl * isl + (spec.lambda_psl * lse if spec.lambda_psl else 0.0))
+            L = spec.lambda_isl * isl + (spec.lambda_psl * lse if spec.lambda_psl else 0.0)
             fp = np.where(mask, spec.lambda_isl * w + spec.lambda_psl * np.exp((x - lse) / T), 0.0)
             G = fp * A / E ** 2 if spec.normalize else fp * A
             g = O.adjoint(s, self.M, G, rows, bins)
             if spec.normalize:
                 g = g - (2.0 / E ** 3) * float(np.sum(fp * chi)) * s
+            if hpsl:
+                # hard PSL from the GLOBAL max and argmax key; the subgradient term is held by
+                # shard 0 only (the sum over shards is the full gradient)
+                L += hpsl * glob[b, 1].item()
+                if shard[0] == 0:
+                    key = int(glob[b, 4].item())
+                    k, m = key // M + self._key_lo(spec), key % M
+                    Ak = O.ambiguity(s, M, rows=np.array([k]), bins=np.array([m]))
+                    Gk = hpsl * (Ak / E ** 2 if spec.normalize else Ak)
+                    g = g + O.adjoint(s, M, Gk, np.array([k]), np.array([m]))
+                    if spec.normalize:
+                        g = g - (2.0 / E ** 3) * hpsl * float(np.abs(Ak[0, 0]) ** 2) * s
+            losses.append(L)
             grads.append(g)
-        return torch.tensor(losses, dtype=torch.float64), torch.tensor(np.stack(grads))
+        lo, go = torch.tensor(losses, dtype=torch.float64), torch.tensor(np.stack(grads))
+        if loss_out is not None:        # in place, like the ABI's caller-owned outputs
+            loss_out.copy_(lo)
+            grad.copy_(go)
+            return loss_out, grad
+        return lo, go
 
 
 class OracleSinglePassBackend(OracleShardBackend):
@@ -115,6 +149,7 @@ class OracleSinglePassBackend(OracleShardBackend):
         return torch.tensor(out, dtype=torch.float64)
 
     def sp_end(self, s_b, M, spec, glob, shard):
+        # (returns NaN loss / zero grad where the rule fails, like the ABI)
         omega, xbar = self._xbar()
         T = spec.temperature
         losses, grads, valid = [], [], []
@@ -145,7 +180,13 @@ def _sp_worker(rank, world, port, case, q):
         be = OracleSinglePassBackend(N, M)
         calls = []
         fwd = be.forward_partials
-        be.forward_partials = lambda *a: (calls.append("two-pass"), fwd(*a))[1]
+
+        def spy(*a, skip=None):
+            # the device-side fallback always runs; it does work only for unskipped waveforms
+            if skip is None or not bool(skip.all()):
+                calls.append("two-pass")
+            return fwd(*a, skip=skip)
+        be.forward_partials = spy
         loss, g = sharding.delay_sharded_loss_grad(torch.tensor(s), M, LossSpec.from_dict(spec_d), backend=be)
         q.put((rank, loss.numpy(), g.numpy(), calls))
     finally:
@@ -209,6 +250,10 @@ def _worker(rank, world, port, case, q):
 
 CASES = [
     (12, 16, dict(k_max=6, d_max=5, ml_k=0, ml_d=0, lambda_isl=1.0, lambda_psl=0.0, normalize=1)),
+    # hard PSL (section-7 loss) needs the global argmax: the two-pass protocol, not the
+    # ISL-only shortcut
+    (12, 16, dict(k_max=6, d_max=5, ml_k=0, ml_d=0, lambda_isl=0.5, lambda_psl=0.0, lambda_hpsl=1.0,
+                  normalize=1)),
     (12, 16, dict(k_max=11, d_max=8, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05, normalize=1)),
     (9, 16, dict(k_max=4, d_max=6, ml_k=1, ml_d=0, lambda_isl=0.0, lambda_psl=1.0, temperature=50.0, normalize=0)),
 ]
@@ -233,6 +278,10 @@ def test_delay_and_batch_sharding_gloo_world2(case):
     refs = [O.loss_and_grad(s[b], M, ospec) for b in range(3)]
     L_ref = np.array([r[0] for r in refs])
     g_ref = np.stack([r[1] for r in refs])
+    if spec_d.get("lambda_hpsl"):
+        hp = [O.hard_psl_and_grad(s[b], M, ospec) for b in range(3)]
+        L_ref = L_ref + spec_d["lambda_hpsl"] * np.array([h[0] for h in hp])
+        g_ref = g_ref + spec_d["lambda_hpsl"] * np.stack([h[1] for h in hp])
     for rank, loss, g, (a, z), lb, gb in res:
         np.testing.assert_allclose(loss, L_ref, rtol=1e-10)
         np.testing.assert_allclose(g, g_ref, atol=1e-10 * np.abs(g_ref).max())
@@ -240,6 +289,39 @@ def test_delay_and_batch_sharding_gloo_world2(case):
         np.testing.assert_allclose(gb, g_ref[a:z], atol=1e-10 * np.abs(g_ref).max())
     blocks = sorted((a, z) for _, _, _, (a, z), _, _ in res)
     assert blocks == [(0, 2), (2, 3)]
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_22935_b200 import sharding
+
+        class Fake:
+            def loss_grad(self, s, M, spec, glob, shard):
+                return s.real.sum(1).double(), s
+        s = torch.arange(7, dtype=torch.float64).to(torch.complex128)[:, None].repeat(1, 3)
+        sl, loss, g = sharding.batch_sharded_loss_grad(s, 4, None, backend=Fake(), gather_loss=True)
+        q.put((rank, loss.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_sharded_gather_loss_unequal_blocks():
+    """B = 7 over 2 ranks (blocks of 4 and 3): the padded all_gather returns the full,
+    correctly ordered loss vector (equal-size collective buffers)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, loss in res:
+        np.testing.assert_array_equal(loss, 3.0 * np.arange(7))
 
 
 def test_batch_slice_partition():
