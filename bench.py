@@ -4,19 +4,27 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl graf|reference]
 
-A step = one forward + loss + gradient pass of the whole hot path (SURVEY.md
-§8(a) rows a0-a7, plus a8 when sharded) over one batch of seeded synthetic
-waveforms of the chosen BASELINE.json config (default: configs[1] = c2, B=256,
-N=M=256, masked ISL, fused single pass), called through the C ABI
-(graf_af_loss_grad).  Inputs are resident in HBM before timing; each timed step
-is a CUDA-graph replay of that call, timed with CUDA events on the launching
-stream, with L2 flushed (256 MiB memset) between steps outside the events.
-Multi-GPU (torchrun): batch sharding, every rank runs its own batch (weak
-scaling, no data-path collective); time = max over ranks.
+A step = one forward + loss + gradient pass of the whole hot path (SURVEY.md §8(a)
+rows a0-a7, plus a8 when sharded) over one batch of seeded synthetic waveforms of the
+chosen BASELINE.json config, called through the C ABI (graf_af_loss_grad).  Default:
+configs[4] = c5 (B = 8, N = M = 16384, full-plane ISL + soft-PSL T = 0.01), the largest
+configuration and the one the north star's fused-loss FP32 target names; c1..c4 are
+behind --config.  Inputs are resident in HBM before timing; each timed step is a
+CUDA-graph replay of that call (eager ABI calls for the NCCL delay-sharded step), timed
+with CUDA events on the launching stream, with L2 flushed (256 MiB memset) between steps
+outside the events.  The dominant kernel's duration is read from events the ABI records
+around its delay-row kernels, in the SAME replays.
 
-`--impl reference`: this build has no reference implementation (the paper
-ships no code); the reference arm is the float64 CPU oracle (oracle/), timed on
-the host cores on a bounded sample of the same workload.
+Multi-GPU (one process per GPU, torchrun; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run), SURVEY.md §8(e):
+  c5      delay sharding: every rank runs its folded rows k = r (mod G) of all 8 waveforms,
+          all_gather of B x 48 B partials + all_reduce of the B x N gradient (NCCL);
+  c2-c4   batch sharding: B/G contiguous waveforms per rank, no collective;
+  c1      replicas (one 64-sample waveform does not shard).
+Time = max over ranks; value = waveforms of the whole job / time.
+
+`--impl reference`: the paper ships no code; the reference arm is the float64 CPU oracle
+(oracle/), timed on the host cores on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -37,10 +45,18 @@ import numpy as np  # noqa: E402
 
 from graf_inputs import CONFIGS, config_waveforms  # noqa: E402
 
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # B200_PROFILING.md: 148 SMs, 1965 MHz; 128 FP32 lanes/SM
+SM_COUNT, SM_MAX_MHZ = 148, 1965.0      # B200_PROFILING.md; the bench reads the live values when it can
+FP32_PEAK_TFLOPS = SM_COUNT * 128 * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 74.4: 128 FP32 lanes/SM x FFMA
+
+
+def fft_stage_flops(M: int) -> float:
+    """Nominal flops of one radix-2 stage of a length-M FFT (5 M log2 M per
+    FFT = 5 M per stage)."""
+    return 5.0 * M
 
 
 def workload(cid: int) -> dict:
+    """The config's step and its algorithmic work (SURVEY.md §8(d) counting rules)."""
     cfg = CONFIGS[cid]
     loss = dict(cfg["loss"])
     note = ""
@@ -50,32 +66,41 @@ def workload(cid: int) -> dict:
         loss["normalize"] = 0
         note = "raw (unnormalised) full-plane ISL: the normalised one is constant (volume identity)"
     N, M, B = cfg["N"], cfg["M"], cfg["B"]
+    L2M = int(math.log2(M))
     rows = min(loss["k_max"], N - 1) + 1                       # folded delay rows k >= 0
-    ffts = 2 if loss["lambda_psl"] == 0 else 3                  # fused ISL: fwd+inv; soft-PSL: fwd | fwd+inv
+    stages = 2 * L2M                                           # fused ISL: forward + inverse FFT
+    count = "2 FFTs per folded row (forward + inverse)"
     single = False
-    if ffts == 3 and not cfg["surface"]:
-        # band cache (graf_api.cu make_plan): a band of <= M/4 bins (cache <= 1 GiB) is kept
-        # from pass 1, so pass 2 runs only the inverse FFT -- count the FFTs actually executed
+    if loss["lambda_psl"] != 0 and not cfg["surface"]:
         nband = 2 * min(loss["d_max"], M // 2) + 1
-        if nband <= M // 4 and B * rows * nband * 8 <= (1 << 30):
-            ffts = 2
-            note = "soft-PSL two-pass with the band cache: pass 2 reuses pass 1's in-band FFT outputs"
         full = (min(loss["k_max"], N - 1) == N - 1 and loss["d_max"] >= M // 2 and loss.get("ml_k", 0) == 0
                 and loss.get("ml_d", 0) == 0 and loss.get("normalize", 1) == 1)
         if full:
-            # full-plane centred soft-PSL (R13): one pass of forward + inverse FFT per row,
-            # guarded fallback passes only for waveforms outside the validity rule
-            ffts = 2
+            # full-plane centred soft-PSL (R13): ONE pass of forward + inverse FFT per row
+            # (the guarded fallback passes exit at once for waveforms inside the rule)
             single = True
             note = "full-plane soft-PSL as one optimistic pass (R13), per-waveform guarded fallback"
-    flops = B * rows * ffts * 5.0 * M * math.log2(M)             # SURVEY.md §8(d) algorithmic FFT flops
+        elif nband <= M // 4 and B * rows * nband * 8 <= (1 << 30):
+            # band cache: pass 2 reuses pass 1's in-band FFT outputs, so a row runs pass 1's
+            # forward FFT and pass 2's inverse.  Both are PRUNED to the band (§8(d): count the
+            # pruned FFT): pass 1's last radix-2 stage keeps 2 of E = 16 outputs per thread
+            # (1/8 of the stage) and its first stage has a zero upper half (2N <= M); pass 2's
+            # first radix-16 pass has 2 nonzero inputs of 16 (its 4 stages cost ~1).
+            stages = (L2M - 1 - 7.0 / 8.0) + (L2M - 3)
+            count = (f"pruned: pass-1 forward {L2M - 1 - 7 / 8:.3f} + pass-2 inverse {L2M - 3} of "
+                     f"{L2M} radix-2 stages (band cache, 2N <= M, band < M/E)")
+            note = "soft-PSL two-pass with the band cache: pass 2 reuses pass 1's in-band FFT outputs"
+        else:
+            stages = 3 * L2M
+            count = "3 FFTs per folded row (pass 1 forward; pass 2 forward + inverse)"
+    flops = B * rows * stages * fft_stage_flops(M)
     surf_bytes = 0
     if cfg["surface"]:
         per = 8 if cfg["surface"] == "c64" else 4
         surf_bytes = B * (2 * N - 1) * M * per
     io_bytes = B * N * 8 * 2
-    return dict(cid=cid, cfg=cfg, loss=loss, N=N, M=M, B=B, rows=rows, ffts=ffts, flops=flops, single=single,
-                surf_bytes=surf_bytes, io_bytes=io_bytes, note=note,
+    return dict(cid=cid, cfg=cfg, loss=loss, N=N, M=M, B=B, rows=rows, stages=stages, flops=flops,
+                flop_count=count, single=single, surf_bytes=surf_bytes, io_bytes=io_bytes, note=note,
                 launches=(2 if loss["lambda_psl"] == 0 else 4))
 
 
@@ -86,6 +111,36 @@ def describe(w: dict) -> str:
             f"{'surface ' + c['surface'] + ' + ' if c['surface'] else ''}"
             f"ISL x{L['lambda_isl']} + softPSL x{L['lambda_psl']} (T={L['temperature']}) on |k|<={L['k_max']}, "
             f"|d|<={L['d_max']} minus |k|<={L['ml_k']}&|d|<={L['ml_d']}, normalize={L['normalize']}")
+
+
+def rank_plan(w: dict, world: int, rank: int, mode: str = "loss_grad") -> dict:
+    """Which waveforms / rows this rank processes and how the job's
+    throughput is counted."""
+    B = w["B"]
+    if world == 1:
+        return dict(kind="single", b0=0, B_local=B, units=B, scaling="strong", shard=(0, 1),
+                    parallelism="1 GPU")
+    if w["cid"] == 5 and mode == "loss_grad":
+        return dict(kind="delay", b0=0, B_local=B, units=B, scaling="strong", shard=(rank, world),
+                    parallelism=f"delay-sharded x{world} (rows k = r mod {world}; NCCL all_gather + all_reduce)")
+    if B >= world:
+        base, rem = divmod(B, world)
+        b0 = rank * base + min(rank, rem)
+        return dict(kind="batch", b0=b0, B_local=base + (1 if rank < rem else 0), units=B, scaling="strong",
+                    shard=(0, 1), parallelism=f"batch-sharded x{world} (B/G contiguous waveforms per rank)")
+    return dict(kind="replica", b0=0, B_local=B, units=B * world, scaling="weak", shard=(0, 1),
+                parallelism=f"replicas x{world} (B = {B} does not shard)")
+
+
+def max_over_ranks(values, dev, world):
+    """Element-wise max over ranks (device-timed numbers: the slowest rank decides)."""
+    if world == 1:
+        return list(values)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(values), dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
 
 
 # ---------------------------------------------------------------------------
@@ -144,96 +199,139 @@ def read_traffic(key: str):
         return None
 
 
-# ---------------------------------------------------------------------------
-def cpu_baseline(w: dict, budget_s: float = 12.0) -> dict:
-    """The float64 oracle as it stands, on the host cores, on a bounded sample."""
-    from oracle import graf_oracle as O
+def host_info() -> dict:
     try:
         from threadpoolctl import threadpool_info
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
         threads = os.cpu_count()
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cores": threads, "nproc": os.cpu_count(), "cpu_model": model}
+
+
+# ---------------------------------------------------------------------------
+def oracle_sample(w: dict, i: int):
+    """One bounded sample of the workload through the float64 oracle, as it stands.
+    Returns the fraction of a waveform's work it covered.  Waveforms whose direct sum
+    takes minutes (N*M > 4096*8192: c5) are sampled by CELLS: the oracle's loss_and_grad
+    over the delay rows |k| <= 63 and centred Doppler bins |d| <= 1023 of waveform i
+    (forward sum, loss terms and adjoint for those cells; its cost per cell is one
+    length-N dot product each way, the same for every cell of the plane)."""
+    from oracle import graf_oracle as O
     spec = O.LossSpec.from_dict(w["loss"])
     N, M = w["N"], w["M"]
-    done, t0 = 0, time.perf_counter()
-    b = 0
+    s = config_waveforms(w["cid"], batch=1, start=i % w["B"])[0]
+    if N * M > 4096 * 8192:
+        sub = O.LossSpec.from_dict(dict(w["loss"], k_max=63, d_max=1023))
+        O.loss_and_grad(s, M, sub)
+        return (127 * 2047) / ((2 * N - 1) * M)
+    if w.get("match"):
+        tgt = np.random.default_rng(i).random((2 * N - 1, M)) / M
+        O.match_loss_and_grad(s, M, spec, tgt, -(N - 1), "centered")
+    elif w.get("cross"):
+        s2 = config_waveforms(w["cid"], batch=1, start=(i + 777) % w["B"])[0]
+        O.cross_loss_and_grad(s, s2, M, spec)
+    else:
+        per = w.get("periodic", False)
+        O.loss_and_grad(s, M, spec, periodic=per)
+        if w["cfg"]["surface"]:
+            O.surface(s, M, w["cfg"]["surface"], "centered", periodic=per,
+                      **(dict(k_begin=-(N // 2), k_end=N // 2) if per else {}))
+    return 1.0
+
+
+def sample_label(w: dict) -> str:
+    if w["N"] * w["M"] > 4096 * 8192:
+        return ("cells |k|<=63 x |d|<=1023 (127 x 2047 of 32767 x 16384) of c5 waveforms, forward + loss + "
+                "adjoint by direct float64 sums")
+    return f"whole {w['cfg']['name']} waveforms, forward + loss + adjoint by direct float64 sums"
+
+
+def cpu_baseline(w: dict, budget_s: float = 15.0) -> dict:
+    """The float64 oracle as it stands, on the host cores, on a bounded sample."""
+    done, t0, i = 0.0, time.perf_counter(), 0
     while True:
-        s = config_waveforms(w["cid"], batch=1, start=b % w["B"])[0]
-        if w["N"] * w["M"] > 4096 * 8192:          # c5: the direct sum takes minutes per waveform
-            s_small = s
-            O.loss_and_grad_chunked(s_small, M, spec)
-        elif w.get("match"):
-            tgt = np.random.default_rng(b).random((2 * N - 1, M)) / M
-            O.match_loss_and_grad(s, M, spec, tgt, -(N - 1), "centered")
-        elif w.get("cross"):
-            s2 = config_waveforms(w["cid"], batch=1, start=(b + 777) % w["B"])[0]
-            O.cross_loss_and_grad(s, s2, M, spec)
-        else:
-            per = w.get("periodic", False)
-            O.loss_and_grad(s, M, spec, periodic=per)
-            if w["cfg"]["surface"]:
-                O.surface(s, M, w["cfg"]["surface"], "centered", periodic=per,
-                          **(dict(k_begin=-(N // 2), k_end=N // 2) if per else {}))
-        done += 1
-        b += 1
+        done += oracle_sample(w, i)
+        i += 1
         el = time.perf_counter() - t0
-        if el > budget_s or done >= w["B"]:
+        if el > budget_s or i >= w["B"] * (1 if done >= i else 50):
             break
-    v = done / el
-    return {"value": v, "unit": "surfaces/s", "cores": threads, "kind": "oracle",
-            "sample": f"{done} of {w['B']} {w['cfg']['name']} waveforms ({el:.1f} s, float64 direct-sum oracle)"}
+    hi = host_info()
+    return {"value": done / el, "unit": "surfaces/s", "cores": hi["cores"], "kind": "oracle",
+            "sample": f"{i} samples = {done:.4g} waveforms in {el:.1f} s: {sample_label(w)}",
+            "nproc": hi["nproc"], "cpu_model": hi["cpu_model"]}
 
 
 def run_reference(args, w) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import graf_oracle as O
-    spec = O.LossSpec.from_dict(w["loss"])
-    per_step = {1: 1, 2: 8, 3: 1, 4: 1, 5: 1}[w["cid"]]
-    if w["cid"] == 5:
-        print(json.dumps({"impl": "reference", "unavailable":
-                          "float64 direct-sum oracle needs ~10 min per c5 waveform (N=M=16384)"}))
-        return
+    per_step = {1: 1, 2: 8, 3: 1, 4: 1, 5: 4}[w["cid"]]
 
     def step(i):
+        d = 0.0
         for j in range(per_step):
-            s = config_waveforms(w["cid"], batch=1, start=(i * per_step + j) % w["B"])[0]
-            per = w.get("periodic", False)
-            if w.get("match"):
-                tgt = np.random.default_rng(j).random((2 * w["N"] - 1, w["M"])) / w["M"]
-                O.match_loss_and_grad(s, w["M"], spec, tgt, -(w["N"] - 1), "centered")
-                continue
-            if w.get("cross"):
-                s2 = config_waveforms(w["cid"], batch=1, start=(j + 777) % w["B"])[0]
-                O.cross_loss_and_grad(s, s2, w["M"], spec)
-                continue
-            O.loss_and_grad(s, w["M"], spec, periodic=per)
-            if w["cfg"]["surface"]:
-                O.surface(s, w["M"], w["cfg"]["surface"], "centered", periodic=per,
-                          **(dict(k_begin=-(w["N"] // 2), k_end=w["N"] // 2) if per else {}))
+            d += oracle_sample(w, i * per_step + j)
+        return d
 
     for i in range(args.warmup):
         step(i)
     t0 = time.perf_counter()
+    done = 0.0
     for i in range(args.steps):
-        step(args.warmup + i)
+        done += step(args.warmup + i)
     el = time.perf_counter() - t0
-    v = per_step * args.steps / el
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
+    v = done / el
+    hi = host_info()
     line = {"metric": "AF forward+loss+grad surfaces/sec", "value": v, "unit": "surfaces/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": describe(w), "sample_per_step": f"{per_step} waveform(s)"},
-            "cpu_baseline": {"value": v, "unit": "surfaces/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{per_step} waveform(s) per step x {args.steps} steps"},
+            "config": {"workload": describe(w), "sample_per_step": f"{per_step} samples: {sample_label(w)}"},
+            "cpu_baseline": {"value": v, "unit": "surfaces/s", "cores": hi["cores"], "kind": "oracle",
+                             "sample": f"{per_step} samples per step x {args.steps} steps = {done:.4g} waveforms: "
+                                       f"{sample_label(w)}", "cpu_model": hi["cpu_model"]},
             "e2e": {"value": v, "unit": "surfaces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def relaunch_under_torchrun(n: int) -> None:
+    """`--gpus N` outside torchrun: re-run this command as N ranks (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
+def measure_fp32_peak(graf, dev, stream) -> dict:
+    """FFMA-bound probe kernel (graf_probe_fp32), CUDA events, best of 5, clocks alongside."""
+    import ctypes
+    import torch
+    L = graf.lib()
+    scratch = torch.empty(4 * 256 * 1024, dtype=torch.float32, device=dev)
+    fl = ctypes.c_double(0.0)
+    best = 0.0
+    with torch.cuda.stream(stream):
+        for it in range(6):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            graf.graf.L.check(L.graf_probe_fp32(ctypes.c_void_p(scratch.data_ptr()), 4096, ctypes.byref(fl),
+                                                ctypes.c_void_p(stream.cuda_stream)))
+            b.record(stream)
+            b.synchronize()
+            if it:
+                best = max(best, fl.value / (a.elapsed_time(b) / 1e3) / 1e12)
+    return {"tflops": best, "how": "graf_probe_fp32: 8 FFMA chains/thread, 4 x 256-thread CTAs per SM, best of 5"}
 
 
 # ---------------------------------------------------------------------------
@@ -242,7 +340,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="graf", choices=["graf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0)
@@ -251,6 +349,11 @@ def main():
     ap.add_argument("--periodic", action="store_true",
                     help="the paper's circular surface (Eq. 2 / Alg. 1, SURVEY 8(f) NEXT-1); needs M == N")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        if world == 1 and args.gpus > 1 and "RANK" not in os.environ:
+            relaunch_under_torchrun(args.gpus)
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world}")
     if args.mode == "lpi":
         return run_lpi(args)
     if args.mode == "mlw":
@@ -262,7 +365,7 @@ def main():
             raise SystemExit("--periodic needs a config with M == N (c1, c2, c3, c5)")
         # folded circular rows k = 0..min(k_max, N/2), same FFT work per row
         w["rows"] = min(w["loss"]["k_max"], w["N"] // 2) + 1
-        w["flops"] = w["B"] * w["rows"] * w["ffts"] * 5.0 * w["M"] * math.log2(w["M"])
+        w["flops"] = w["B"] * w["rows"] * w["stages"] * fft_stage_flops(w["M"])
         if w["cfg"]["surface"]:
             w["surf_bytes"] = w["B"] * w["N"] * w["M"] * (8 if w["cfg"]["surface"] == "c64" else 4)
         w["note"] = (w["note"] + "; " if w["note"] else "") + "periodic (circular) surface, paper Eq. 2 / Alg. 1"
@@ -271,6 +374,7 @@ def main():
             raise SystemExit("--mode forward needs a config with a surface (c1, c3)")
         # folded rows covering the whole surface window, one forward FFT each
         w["flops"] = w["B"] * (w["N"] // 2 + 1 if args.periodic else w["N"]) * 5.0 * w["M"] * math.log2(w["M"])
+        w["flop_count"] = "1 forward FFT per folded row"
         w["io_bytes"] = w["B"] * w["N"] * 8
         w["launches"] = 1
         w["note"] = "full-surface mode: graf_af_forward writes the surface; no loss or gradient"
@@ -279,9 +383,9 @@ def main():
         # pass streaming a per-waveform fp32 target of the full surface window
         w["loss"] = dict(w["loss"], lambda_isl=0.0, lambda_psl=0.0, normalize=1)
         w["match"] = True
-        w["ffts"] = 2
         w["rows"] = min(w["loss"]["k_max"], w["N"] - 1) + 1
         w["flops"] = w["B"] * w["rows"] * 2 * 5.0 * w["M"] * math.log2(w["M"])
+        w["flop_count"] = "2 FFTs per folded row (forward + inverse)"
         # algorithmic bytes: s + g + the target cells of the region (both mirrored rows)
         w["surf_bytes"] = w["B"] * (2 * w["rows"] - 1) * min(w["M"], 2 * w["loss"]["d_max"] + 1) * 4
         w["launches"] = 2
@@ -291,18 +395,21 @@ def main():
         # X = sum s1 conj(s2(n-k)) W^{mn}, rows unfolded (no mirror symmetry)
         w["cross"] = True
         w["rows"] = 2 * min(w["loss"]["k_max"], w["N"] - 1) + 1
-        w["flops"] = w["B"] * w["rows"] * w["ffts"] * 5.0 * w["M"] * math.log2(w["M"])
+        w["flops"] = w["B"] * w["rows"] * w["stages"] * fft_stage_flops(w["M"])
         w["io_bytes"] = w["B"] * w["N"] * 8 * 4
         w["note"] = "cross-ambiguity of (s1, s2) pairs, unfolded rows; loss/grad w.r.t. both"
     if args.impl == "reference":
         return run_reference(args, w)
+    run_graf(args, w, world)
 
+
+def run_graf(args, w, world):
+    import ctypes
     import torch
     import torch.distributed as dist
 
     import paper_2506_22935_b200 as graf
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
@@ -311,9 +418,12 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     W = max(3, args.warmup)
+    plan = rank_plan(w, world, rank, args.mode)
+    delay = plan["kind"] == "delay"
 
-    B, N, M = w["B"], w["N"], w["M"]
-    s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=rank * B)).pin_memory()
+    N, M = w["N"], w["M"]
+    B = plan["B_local"]                                   # waveforms this rank processes
+    s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=plan["b0"])).pin_memory()
     s = s_host.to(dev)
     spec = graf.LossSpec.from_dict(w["loss"])
     out = w["cfg"]["surface"]
@@ -321,8 +431,11 @@ def main():
         out = None
         spec.lambda_match = 1.0
         g_ = torch.Generator(device=dev)
-        g_.manual_seed(1234 + rank)
+        g_.manual_seed(1234 + plan["b0"])
         spec.target = torch.rand((B, 2 * N - 1, M), generator=g_, device=dev) * (1.0 / M)
+    if w.get("cross"):
+        s2_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=plan["b0"] + 777)).pin_memory()
+        s2 = s2_host.to(dev)
     ws = graf.graf.Workspace()
     grad = torch.empty((B, N), dtype=torch.complex64, device=dev)
     loss_out = torch.empty((B,), dtype=torch.float64, device=dev)
@@ -334,55 +447,43 @@ def main():
         surf = torch.empty((B, nrows, M), dtype=torch.complex64 if out == "c64" else torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
-    ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    delay = (w["cid"] == 5 and world > 1)   # c5: delay-axis sharding with NCCL exchange (strong scaling)
+    L = graf.lib()
+    graf.graf.L.check(L.graf_init(ctypes.c_void_p(stream.cuda_stream)))
     if delay:
         from paper_2506_22935_b200 import sharding
-        s_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=0)).pin_memory()
-        s = s_host.to(dev)
+        tb = TimedBackend(graf, sharding)
 
-    if w.get("cross"):
-        s2_host = torch.from_numpy(config_waveforms(w["cid"], batch=B, start=rank * B + 777)).pin_memory()
-        s2 = s2_host.to(dev)
-
-    def call(st=None):
+    def call(st, sd=None):
+        sd = s if sd is None else sd
         if w.get("cross"):
-            graf.xaf_loss_grad(s, s2, M, spec, ws=ws, stream=st)
-            return
+            return graf.xaf_loss_grad(sd, s2, M, spec, ws=ws, stream=st)
         if delay:
-            sharding.delay_sharded_loss_grad(s, M, spec, backend=tb)
-            return
+            return sharding.delay_sharded_loss_grad(sd, M, spec, backend=tb)
         if args.mode == "forward":
-            graf.af_forward(s, M, out=out, layout="centered", ws=ws, surface=surf, stream=st, **kb)
-            return
-        graf.af_loss_grad(s, M, spec, out=out, layout="centered", ws=ws, grad=grad, loss_out=loss_out,
-                          surface=surf, stream=st, **kb)
+            return graf.af_forward(sd, M, out=out, layout="centered", ws=ws, surface=surf, stream=st, **kb)
+        return graf.af_loss_grad(sd, M, spec, out=out, layout="centered", ws=ws, grad=grad, loss_out=loss_out,
+                                 surface=surf, stream=st, **kb)
 
     with torch.cuda.stream(stream):
-        call(stream)                                    # twiddle init + workspace, before capture
+        call(stream)                                    # workspace + attributes, before capture
+        call(stream)
     torch.cuda.synchronize()
-    L = graf.lib()
-    launches_per_step = int(L.graf_last_launch_count())   # device ops the ABI call enqueued
-    # the dominant kernel(s) are bracketed by events the ABI records around its
-    # delay-row kernels (graf_set_profile_events); recorded into the captured graph,
-    # so the kernel time comes from the same graph replays as the step time
+    launches_per_step = int(L.graf_last_launch_count())   # device ops one ABI call enqueues
+    ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev_k0.record(stream)        # torch creates the CUDA events lazily on first record
     ev_k1.record(stream)
     torch.cuda.synchronize()
     if delay:
-        tb = TimedBackend(graf, sharding)
-        class _Eager:                     # NCCL step: eager replay (no graph)
+        class _Eager:                     # NCCL step: eager ABI calls (no host sync inside)
             def replay(self_inner):
                 call(stream)
         g = _Eager()
     else:
-        g = torch.cuda.CUDAGraph()               # the timed step (no event nodes)
+        # the timed graph: the ABI records ev_k0 / ev_k1 (external event nodes) around its
+        # delay-row kernels, so step and kernel times come from the same replays
+        g = torch.cuda.CUDAGraph()
+        L.graf_set_profile_events(ctypes.c_void_p(ev_k0.cuda_event), ctypes.c_void_p(ev_k1.cuda_event))
         with torch.cuda.graph(g, stream=stream):
-            call(stream)
-        g_k = torch.cuda.CUDAGraph()             # the same call with the kernel events recorded
-        L.graf_set_profile_events(ctypes_ptr(ev_k0), ctypes_ptr(ev_k1))
-        with torch.cuda.graph(g_k, stream=stream):
             call(stream)
         L.graf_set_profile_events(None, None)
     torch.cuda.synchronize()
@@ -394,54 +495,32 @@ def main():
             g.replay()
         t_end = time.time() + args.settle_s          # bring clocks to load before timing
         while time.time() < t_end:
-            for _ in range(20):
+            for _ in range(5 if w["cid"] in (3, 5) else 20):
                 g.replay()
             stream.synchronize()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kern_ms = []
+    step_ms, kern_ms = [], []
     with torch.cuda.stream(stream):
         for i in range(args.steps):
             flush.zero_()
-            ev_a[i].record(stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
             g.replay()
-            ev_b[i].record(stream)
-        ev_b[-1].synchronize()
+            b.record(stream)
+            b.synchronize()
+            step_ms.append(a.elapsed_time(b))
+            kern_ms.append(tb.kernel_ms() if delay else ev_k0.elapsed_time(ev_k1))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]
-    # dominant kernel(s): ev_k0/ev_k1 around the delay-row kernels, same inputs, same
-    # L2 flush protocol (graph replays; eager ABI calls for the NCCL-sharded step)
-    if delay:
-        with torch.cuda.stream(stream):
-            for i in range(args.steps):
-                flush.zero_()
-                call(stream)
-                torch.cuda.synchronize()
-                kern_ms.append(tb.kernel_ms())
-    else:
-        with torch.cuda.stream(stream):
-            for i in range(args.steps):
-                flush.zero_()
-                g_k.replay()
-                ev_k1.synchronize()
-                kern_ms.append(ev_k0.elapsed_time(ev_k1))
-    total_ms = sum(step_ms)
-    kern_avg = sum(kern_ms) / len(kern_ms)
-    if world > 1:
-        t = torch.tensor([total_ms, kern_avg], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, kern_avg = t.tolist()
+    total_ms, kern_avg = max_over_ranks([sum(step_ms), sum(kern_ms) / len(kern_ms)], dev, world)
     ms_per_step = total_ms / args.steps
-    units = B if delay else world * B           # delay sharding: the ranks share one batch
-    value = units * args.steps / (total_ms / 1e3)
+    value = plan["units"] * args.steps / (total_ms / 1e3)
 
     # ---- e2e: public API, pinned host buffers, H2D + call + D2H inside the timed region
     g_host = torch.empty((B, N), dtype=torch.complex64).pin_memory()
@@ -455,58 +534,49 @@ def main():
             a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             s_dev2.copy_(s_host, non_blocking=True)
-            if w.get("cross"):
-                lo, gr, gr2, _ = graf.xaf_loss_grad(s_dev2, s2, M, spec, ws=ws, stream=stream)
-            elif delay:
-                lo, gr = sharding.delay_sharded_loss_grad(s_dev2, M, spec)
-            elif args.mode == "forward":
-                sf, _ = graf.af_forward(s_dev2, M, out=out, layout="centered", ws=ws, surface=surf, stream=stream,
-                                        **kb)
+            if args.mode == "forward":
+                sf, _ = call(stream, s_dev2)
                 zrow = sf[:, N // 2 if args.periodic else N - 1, :]   # zero-delay cut of every surface
                 if zrow_host is None:
                     zrow_host = torch.empty(zrow.shape, dtype=zrow.dtype).pin_memory()
                 zrow_host.copy_(zrow, non_blocking=True)
-                b_.record(stream)
-                b_.synchronize()
-                if i >= W:
-                    e2e_ms.append(a.elapsed_time(b_))
-                continue
             else:
-                lo, gr, _ = graf.af_loss_grad(s_dev2, M, spec, out=out, layout="centered", ws=ws, surface=surf,
-                                              stream=stream, **kb)
-            l_host.copy_(lo, non_blocking=True)
-            g_host.copy_(gr, non_blocking=True)
+                r = call(stream, s_dev2)
+                lo, gr = r[0], r[1]
+                l_host.copy_(lo, non_blocking=True)
+                g_host.copy_(gr, non_blocking=True)
             b_.record(stream)
             b_.synchronize()
             if i >= W:
                 e2e_ms.append(a.elapsed_time(b_))
-    e2e_total = sum(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = t.item()
-    e2e_value = units * len(e2e_ms) / (e2e_total / 1e3)
+    e2e_total = max_over_ranks([sum(e2e_ms)], dev, world)[0]
+    e2e_value = plan["units"] * len(e2e_ms) / (e2e_total / 1e3)
 
-    # ---- roofline of the dominant kernel (af_rows_kernel), per launch window
+    # ---- roofline of the dominant kernel(s) (af_rows_kernel), per launch window
     t_k = kern_avg / 1e3
-    if delay:
-        w["flops"] = w["flops"] / world       # this rank's delay rows
-    fl_tf = w["flops"] / t_k / 1e12
-    hbm = None
+    flops_k = w["flops"] * B / w["B"] / (world if delay else 1)     # this rank's rows / waveforms
+    fl_tf = flops_k / t_k / 1e12
     try:
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     except Exception:
-        hbm = 6650.0
-    bytes_k = w["surf_bytes"] + w["io_bytes"]
-    t_alu = w["flops"] / (FP32_PEAK_TFLOPS * 1e12)
+        hbm, hbm_src = 6533.8, "fallback: round-1 MEASURED_PEAKS.json hbm_gbs"
+    bytes_k = (w["surf_bytes"] + w["io_bytes"]) * B / w["B"]
+    t_alu = flops_k / (FP32_PEAK_TFLOPS * 1e12)
     t_hbm = bytes_k / (hbm * 1e9)
+    fp32_meas = measure_fp32_peak(graf, dev, stream) if rank == 0 else None
     if t_hbm > t_alu:
         roof = {"bound": "hbm", "achieved": bytes_k / t_k / 1e9, "peak": hbm, "unit": "GB/s",
-                "frac": bytes_k / t_k / 1e9 / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+                "frac": bytes_k / t_k / 1e9 / hbm, "peak_source": hbm_src}
     else:
         roof = {"bound": "alu", "achieved": fl_tf, "peak": round(FP32_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
                 "frac": fl_tf / FP32_PEAK_TFLOPS,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 flop x 1965 MHz (B200_PROFILING.md)"}
+                "peak_source": "derived (DESIGN.md §5): 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x 1965 MHz",
+                "flop_count": w["flop_count"]}
+        if fp32_meas:
+            roof["peak_measured"] = round(fp32_meas["tflops"], 2)
+            roof["frac_of_measured"] = fl_tf / fp32_meas["tflops"]
+            roof["peak_measured_how"] = fp32_meas["how"]
     roof["traffic"] = read_traffic(f"{w['cid']}{'fwd' if args.mode == 'forward' else ''}"
                                    f"{'per' if args.periodic else ''}{args.mode if args.mode in ('match', 'cross') else ''}")
     two_pass = " (single pass + guarded fallback)" if w.get("single") else " (pass 1 + reduce + pass 2)"
@@ -514,7 +584,7 @@ def main():
                       + (" with the fused cluster finalize" if launches_per_step == 1 and args.mode != "forward"
                          else ""))
     roof["kernel_ms"] = kern_avg
-    roof["algorithmic_flops_per_launch"] = w["flops"]
+    roof["algorithmic_flops_per_launch"] = flops_k
     roof["algorithmic_bytes_per_launch"] = bytes_k
     roof["share_of_step"] = kern_avg / ms_per_step
     cpu = None
@@ -524,15 +594,16 @@ def main():
         line = {"metric": ("AF forward+loss+grad surfaces/sec" if args.mode != "forward"
                            else "AF forward (full-surface) surfaces/sec"), "value": value, "unit": "surfaces/s",
                 "n_gpus": world, "steps": args.steps, "warmup": W, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "strong" if delay else "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": plan["scaling"], "vs_baseline": None,
                 "dtype": "f32",
                 "data": "synthetic",
-                "config": {"workload": describe(w), "B_per_gpu": B, "N": N, "M": M,
+                "config": {"workload": describe(w), "B": w["B"], "B_per_gpu": B, "N": N, "M": M,
                            "cells_per_s": value * N * M,
-                           "parallelism": (f"delay-sharded x{world} (NCCL all_gather + all_reduce)" if delay
-                                           else f"batch-sharded x{world} (weak)"),
+                           "parallelism": plan["parallelism"],
                            "l2": "flushed between steps (256 MiB memset, outside the events)",
-                           "timing": "CUDA-graph replay of graf_af_loss_grad per step, CUDA events",
+                           "timing": ("eager ABI calls per step (NCCL delay sharding), CUDA events" if delay else
+                                      "CUDA-graph replay of the ABI call per step, CUDA events; the kernel "
+                                      "window is timed inside the same replays"),
                            "note": w["note"]},
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "surfaces/s", "h2d_bytes_per_step": B * N * 8,
@@ -541,7 +612,7 @@ def main():
                         "path": ("pinned host s -> H2D -> graf.af_loss_grad (C ABI) -> D2H loss + grad"
                                  if args.mode != "forward" else
                                  "pinned host s -> H2D -> graf.af_forward (C ABI) -> D2H zero-delay cut")},
-                "gpu_launches": ((w["launches"] + 1) if delay else launches_per_step) * args.steps,
+                "gpu_launches": (tb.launches if delay else launches_per_step) * args.steps,
                 "clocks": clocks}
         print(json.dumps(line))
     if world > 1:
@@ -660,32 +731,46 @@ def run_mlw(args):
 
 
 class TimedBackend:
-    """sharding backend that brackets each ABI call's delay-row kernels with events."""
+    """sharding backend that brackets each ABI call's delay-row kernels with events and
+    counts the device operations the ABI enqueues per step."""
 
     def __init__(self, graf, sharding):
         import torch
         self.inner = sharding.GrafBackend()
         self.L = graf.lib()
-        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         for e in self.ev:
             e.record()
         torch.cuda.synchronize()
+        self.launches = 0
+        self._n = 0
+        self._used, self.used = set(), set()
 
-    def _timed(self, i, fn, *a):
+    def _timed(self, i, fn, *a, **kw):
+        self._used.add(i)
         self.L.graf_set_profile_events(ctypes_ptr(self.ev[2 * i]), ctypes_ptr(self.ev[2 * i + 1]))
         try:
-            return fn(*a)
+            return fn(*a, **kw)
         finally:
             self.L.graf_set_profile_events(None, None)
+            self._count()
 
-    def forward_partials(self, *a):
-        return self._timed(0, self.inner.forward_partials, *a)
+    def _count(self):
+        self._n += int(self.L.graf_last_launch_count())
 
-    def loss_grad(self, *a):
-        return self._timed(1, self.inner.loss_grad, *a)
+    def forward_partials(self, *a, **kw):
+        return self._timed(1, self.inner.forward_partials, *a, **kw)
+
+    def loss_grad(self, *a, **kw):
+        r = self._timed(2, self.inner.loss_grad, *a, **kw)
+        self.launches, self._n = self._n, 0          # loss_grad closes a step
+        self.used, self._used = self._used, set()
+        return r
 
     def combine(self, *a):
-        return self.inner.combine(*a)
+        r = self.inner.combine(*a)
+        self._count()
+        return r
 
     # delay-sharded single pass (full-plane soft-PSL, c5): phase 1 holds the row kernels
     def single_pass_eligible(self, *a):
@@ -695,19 +780,17 @@ class TimedBackend:
         return self._timed(0, self.inner.sp_begin, *a)
 
     def sp_end(self, *a):
-        return self.inner.sp_end(*a)
+        r = self.inner.sp_end(*a)
+        self._count()
+        return r
 
     def kernel_ms(self):
-        return self.ev[0].elapsed_time(self.ev[1]) + self.ev[2].elapsed_time(self.ev[3])
+        return sum(self.ev[2 * i].elapsed_time(self.ev[2 * i + 1]) for i in sorted(self.used))
 
 
 def ctypes_ptr(ev):
     import ctypes
     return ctypes.c_void_p(ev.cuda_event)
-
-
-def ctypes_null():
-    return None
 
 
 if __name__ == "__main__":

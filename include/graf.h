@@ -286,6 +286,13 @@ int32_t graf_last_launch_count(void);
  * cudaEventElapsedTime (works inside CUDA-graph capture).  (NULL, NULL) = off. */
 graf_status graf_set_profile_events(void* start, void* stop);
 
+/* Diagnostics: FP32 peak probe.  Enqueues one FFMA-bound kernel (8 independent fmaf chains
+ * per thread, 4 CTAs x 256 threads per SM, `iters` x 16 x 8 FFMA per thread) and writes its
+ * flop count to *flops (host).  The caller times it with events on `stream`; bench.py uses
+ * it as the MEASURED FP32 denominator next to the derived 2 x 128 x SMs x clock.
+ * scratch: device float [4 x SMs x 256] (written only in a practically impossible case). */
+graf_status graf_probe_fp32(float* scratch, int32_t iters, double* flops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_wo
            "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
            "graf_phase_adam_step", "graf_xaf_workspace_bytes", "graf_xaf_forward", "graf_xaf_loss_grad",
            "graf_xaf_backward", "graf_mainlobe_width", "graf_af_single_pass_eligible",
-           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end", "graf_init")
+           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end", "graf_init", "graf_probe_fp32")
 
 
 class AfDesc(ctypes.Structure):
@@ -106,6 +106,8 @@ def lib() -> ctypes.CDLL:
                                              c_int32, c_int32, c_void_p]
         L.graf_init.restype = c_int32
         L.graf_init.argtypes = [c_void_p]
+        L.graf_probe_fp32.restype = c_int32
+        L.graf_probe_fp32.argtypes = [c_void_p, c_int32, POINTER(c_double), c_void_p]
         L.graf_phase_adam_step.restype = c_int32
         L.graf_phase_adam_step.argtypes = [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                            c_void_p, c_float, c_float, c_float, c_float, c_void_p]

@@ -1016,6 +1016,39 @@ graf_status graf_xaf_backward(const graf_af_desc* af, const void* s1, const void
   return impl_backward(cx, af, s1, dA, grad1, ws, ws_bytes, stream);
 }
 
+// FP32 peak probe (bench.py's measured ALU denominator): every thread runs 8 independent
+// FFMA chains for `iters` iterations, 2 flops per FFMA; the chains' sum is written so
+// nothing is optimised away.  Grid: 4 CTAs of 256 threads per SM.
+__global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters, float b) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (float)(threadIdx.x + i) * 1e-3f;
+  const float c = 0.5f * b;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fmaf(a[i], b, c);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 1234.5f) out[blockIdx.x * blockDim.x + threadIdx.x] = s;   // (practically never)
+}
+
+graf_status graf_probe_fp32(float* scratch, int32_t iters, double* flops, void* stream) {
+  t_launches = 0;
+  if (!scratch || iters < 1 || !flops) return fail(GRAF_EINVAL, "scratch / flops NULL or iters < 1");
+  const int blocks = device_sm_count() * 4;
+  fp32_probe_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(scratch, iters, 0.999f);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "fp32_probe_kernel launch");
+  ++t_launches;
+  *flops = 2.0 * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
+  return GRAF_OK;
+}
+
 graf_status graf_set_profile_events(void* start, void* stop) {
   if ((start == nullptr) != (stop == nullptr)) return fail(GRAF_EINVAL, "set both events or neither");
   t_prof_start = static_cast<cudaEvent_t>(start);

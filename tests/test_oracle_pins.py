@@ -611,3 +611,30 @@ def test_mainlobe_width_pins(periodic):
     Wc, gc = O.mainlobe_width_and_grad(one, gamma=1e3, periodic=False)
     t = np.arange(-15, 16)
     assert abs(Wc - float(np.sum(np.abs(t)[(16 - np.abs(t)) ** 2 > 128]))) < 1e-9
+
+
+def test_c5_golden_pinned_by_invariants():
+    """tests/golden/c5_w0_softpsl.npz (scripts/make_c5_golden.py, oracle only) against what
+    the mathematics fixes at N = M = 16384: it was computed from config 5's waveform 0;
+    full-plane normalised ISL = M - 1 (volume identity); max x <= softPSL <=
+    max x + T log|Omega| (|Omega| = (2N-1)M - 1); and the gradient invariants of an
+    |A|-based normalised loss: Im<g,s> = 0 (global phase), Re<g,s> = 0 (scale),
+    Im sum_n n conj(g[n]) s[n] = 0 (linear phase = Doppler shift)."""
+    import hashlib
+    import os
+    from graf_inputs import config_waveforms
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "c5_w0_softpsl.npz"))
+    s = config_waveforms(5, batch=1)[0]
+    assert str(z["s_sha256"]) == hashlib.sha256(np.ascontiguousarray(s).tobytes()).hexdigest()
+    N = M = 16384
+    assert int(z["count"]) == (2 * N - 1) * M - 1
+    assert abs(float(z["isl"]) - (M - 1)) < 1e-9 * M
+    c, lse, T = float(z["c"]), float(z["lse"]), float(z["temperature"])
+    assert c <= lse <= c + T * np.log(float(z["count"]))
+    g = z["grad"]
+    sd = s.astype(np.complex128)
+    scale = np.sum(np.abs(g) * np.abs(sd))
+    n = np.arange(N)
+    assert abs(np.vdot(g, sd).imag) < 1e-12 * scale
+    assert abs(np.vdot(g, sd).real) < 1e-11 * scale
+    assert abs(np.sum(n * np.conj(g) * sd).imag) < 1e-12 * np.sum(n * np.abs(g) * np.abs(sd))
