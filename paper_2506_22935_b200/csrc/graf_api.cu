@@ -228,10 +228,11 @@ void folded_window(int kb, int ke, int* lo, int* hi) {
 
 enum class Kind { Forward, LossGrad, Backward };
 
-// elements of one global s copy (pad_s_kernel): B rows of NL + M, NL = N rounded up to
-// even, plus N + 2 of tail slack (kept even so the second copy starts 16-byte aligned)
+// elements of one global s copy (pad_s_kernel): B rows of NL + M + 2, NL = N rounded up to
+// even (the +2 holds s[N-1] of the shifted copy when N == M), plus N + 2 of tail slack
+// (kept even so the second copy starts 16-byte aligned)
 size_t spad_elems(long long B, int N, int M) {
-  return (size_t)B * (size_t)(N + (N & 1) + M) + (size_t)(N + (N & 1) + 2);
+  return (size_t)B * (size_t)(N + (N & 1) + M + 2) + (size_t)(N + (N & 1) + 2);
 }
 
 Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool cross = false) {
@@ -326,7 +327,7 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   pl.off_comb = off;
   off = align256(off + 2 * sizeof(graf_partials) * (size_t)B);   // combined partials (+ fallback set)
   pl.off_spad = off;
-  // pad_s_kernel rows (NL + M each, NL = N rounded up to even), twice (the second copy
+  // pad_s_kernel rows (NL + M + 2 each, NL = N rounded up to even), twice (the second copy
   // shifted by one sample), each + tail slack: the adjoint's negative-delay rows read (and
   // mask) up to N samples past a row's end
   if (!ci.s_smem) off = align256(off + 2 * sizeof(float2) * spad_elems(B, N, af->m));

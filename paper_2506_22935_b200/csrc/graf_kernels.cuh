@@ -516,10 +516,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const int NP2X = (2 * N + M + 1) & ~1;
   float2* xch = s2_pad + (CROSS ? NP2X : 0);
   float2* gacc_sh = xch + S * XS;
-  // global copy (M = 16384): rows of NL + M with NL = N rounded up to even, so every
-  // row and the sample origin are 16-byte aligned (the SPLIT path loads sample pairs)
+  // global copy (M = 16384): rows of NL + M + 2 with NL = N rounded up to even, so every
+  // row and the sample origin are 16-byte aligned (the SPLIT path loads sample pairs); the
+  // 2 extra keep s[N-1] inside the row of the shifted copy when N == M
   const int NL = N + (N & 1);
-  const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * (NL + M) + NL;
+  const size_t RP = (size_t)(NL + M + 2);
+  const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * RP + NL;
   // zero-padded Doppler axis (2N <= M, aperiodic): time slots e >= E/2 hold n >= M/2 >= N
   // (compiled for M >= 2048 only: the extra code path measured 3 % slower at M = 1024)
   constexpr bool kHalfSizes = (M >= 2048) && !SPLIT;
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const bool eb = FWD ? (kHalfSizes && p.d_max < T) : edge_band;
   constexpr bool kEdgeFwd = kHalfSizes && FWD && num_passes(M, E) >= 3 && !Twiddles<C::MX, E2>::CACHE;
   // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
-  const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * (NL + M) + NL + 1;
+  const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * RP + NL + 1;
   const float2* sv2 = CROSS ? s2_pad + N : sv;               // the conjugated (shifted) factor
   // per-slot accumulator stride: N, or 2N with N zero-padding on the left (p.gpad: folded
   // rows with M == N need no support predicates, out-of-support terms land in the pad)
@@ -732,6 +734,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const float4* c4 = reinterpret_cast<const float4*>((k & 1) == 0 ? c : sv_o + 2 * t - k);
 #pragma unroll
         for (int e = 0; e < E2; ++e) {
+#ifdef GRAF_ABL_NO_LAG   // timing ablation only (scripts/tune.py): no loads, synthetic row
+          v[e] = make_float2(1e-3f * (float)(t + e), 1e-3f);
+          v[e + E2] = make_float2(1e-3f, 1e-3f * (float)e);
+          continue;
+#endif
           // pairs outside the row's support [lo, hi) are zero: no loads (about half of
           // the pairs of a full-plane row)
           if ((((vmask >> e) | (vmask >> (e + E2))) & 1) == 0) {
@@ -754,7 +761,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         }
         else row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
       } else {
+#ifndef GRAF_ABL_NO_FWD   // timing ablation only
         row_fft<M, E, SPLIT, false>(v, sh, t, tw, sync, wt);
+#endif
       }
       asm volatile("" ::: "memory");
       if (FWD && p.cache == 1 && lrow) {
@@ -993,7 +1002,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           if (edge_band) ifft_band_edges<M, E>(v, sh, t, tw, sync);
           else row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
         } else {
+#ifndef GRAF_ABL_NO_INV   // timing ablation only
           row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
+#endif
         }
         // keep the correlation's loads below the last inverse pass
         asm volatile("" ::: "memory");
@@ -1041,6 +1052,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
             for (int e = 0; e < E; ++e) g2[toff(e)] = cadd(g2[toff(e)], cmulc(s2[toff(e)], v[e]));
           }
+#ifdef GRAF_ABL_NO_CORR
+        } else if constexpr (SPLIT) {   // timing ablation only: keep v live, skip the correlation
+          if (v[0].x == 1234.5f) gacc[t] = v[1];
+#endif
         } else if constexpr (SPLIT && !CROSS) {
           // SPLIT rows: process the slot pairs (j, j + E2) = samples (2(t + jT), 2(t + jT) + 1)
           // together so the global s reads are 16-byte pair loads (term 2 always, term 1
@@ -1271,14 +1286,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #ifdef GRAF_API_UNIT   // the reductions and small kernels live in the ABI unit only
 // zero-padded copy of s for the global-memory path: s_pad[b][i] = s[b][i - N] for
 // i in [N, 2N), 0 elsewhere in [0, N + M)
-// rows of NL + M samples, NL = N rounded up to even: s[n] at NL + n, zeros elsewhere
+// rows of NL + M + 2 samples, NL = N rounded up to even: s[n] at NL + n, zeros elsewhere
 // (periodic: s[n + N] at NL + n for -N <= n < 0), so row starts and the origin are 16-byte
 // aligned.  s_pad1 holds the same rows shifted by one sample (s[n] at NL + 1 + n), so a
 // pair starting at an odd sample index is aligned there.
 __global__ void pad_s_kernel(const float2* s, float2* s_pad, float2* s_pad1, int N, int M, long long B,
                              int periodic) {
   const int NL = N + (N & 1);
-  const long long R = NL + M;
+  const long long R = NL + M + 2;
   const long long total = B * R;
   auto val = [&](long long b, int n) {
     if (n >= 0 && n < N) return s[b * N + n];

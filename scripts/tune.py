@@ -16,7 +16,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VDIR = os.path.join(ROOT, "build", "variants")
+VDIR = os.path.join(ROOT, "paper_2506_22935_b200", "variants")   # in-tree: travels with gpurun
 
 
 def build(cfg, specs):
@@ -30,7 +30,7 @@ def build(cfg, specs):
         out = os.path.join(VDIR, f"libgraf_c{cfg}_{tag}.so")
         try:
             _build.compile_link(out, srcs, defines=[f"GRAF_ONLY_M={M}"] + [d for d in defs.split(",") if d],
-                                objdir=os.path.join(VDIR, "obj_" + tag))
+                                objdir=os.path.join(ROOT, "build", "variants", "obj_" + tag))
             print(tag, "rc 0")
         except Exception as e:   # noqa: BLE001
             print(tag, "failed", e)

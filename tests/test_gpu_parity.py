@@ -362,3 +362,22 @@ def test_m16384_backward(layout):
     G = dA[0] if layout == "raw" else np.roll(dA[0], -(M // 2), axis=1)
     ref = O.adjoint(s[0], M, G.astype(np.complex128), rows)
     assert np.abs(g[0] - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("kb,ke", [(-16383, -16370), (-8193, -8180), (16371, 16384)])
+def test_m16384_backward_full_length_edges(kb, ke):
+    """graf_af_backward at N = M = 16384 (the split kernel with the global s copies) on
+    delay windows at both ends, odd and even rows: the last sample s[N-1] is read from the
+    shifted copy for odd negative delays (round-2 fix: rows of NL + M + 2).  dA is nonzero
+    on 64 random Doppler bins so the oracle's DFT matrix stays small."""
+    N = M = 16384
+    s = cg(1, N, 21)
+    rows = np.arange(kb, ke)
+    rng = np.random.default_rng(3)
+    bins = np.sort(rng.choice(M, 64, replace=False))
+    G = cg(1, len(rows) * 64, 22).reshape(len(rows), 64)
+    dA = np.zeros((1, len(rows), M), np.complex64)
+    dA[0][:, bins] = G
+    g = graf.af_backward(dev(s), M, dev(dA), k_begin=kb, k_end=ke, layout="raw").cpu().numpy()
+    ref = O.adjoint(s[0], M, G.astype(np.complex128), rows, bins)
+    assert np.abs(g[0] - ref).max() <= 1e-4 * np.abs(ref).max()
