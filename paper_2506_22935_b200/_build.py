@@ -47,7 +47,8 @@ def up_to_date(lib: str = LIB) -> bool:
 
 def compile_link(out: str, sources, defines=(), objdir=None, verbose=False) -> None:
     """Compile `sources` in parallel to objects and link them into `out`."""
-    objdir = objdir or os.path.join(os.path.dirname(PKG), "build", "obj", os.path.basename(out))
+    # objects stay outside the repo (only the linked .so travels to the GPU box)
+    objdir = objdir or os.path.join(os.environ.get("GRAF_OBJ_DIR", "/tmp/graf_build"), "obj", os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     procs, objs = [], []
     for src in sources:

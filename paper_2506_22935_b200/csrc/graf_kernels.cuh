@@ -102,20 +102,26 @@ struct RowParams {
 
 template <int M>
 struct Cfg;
+#ifndef GRAF_SPLIT_16384
+#define GRAF_SPLIT_16384 0   // 1 = round-1 A/B build: the radix-2 split with the smem accumulator
+#endif
 // E = values per thread, T = threads per row slot, S = row slots per CTA.
-// SPLIT (M = 16384): the row FFT runs as a radix-2 split into two M/2-point
-// sub-FFTs that share one M/2 exchange buffer, so the gradient accumulator fits
-// in shared memory next to it (s is then read from a zero-padded global copy).
+// M = 16384: one 16384-point Stockham FFT per row (E = 32, passes 32 x 32 x 16, a 132 KiB
+// exchange buffer) with the gradient accumulator in TENSOR MEMORY (G_TMEM: 128 KiB of the
+// SM's 256 KiB TMEM, thread-private columns), s read from a zero-padded global copy.
+// (SPLIT, the round-1 layout kept for A/B builds: a radix-2 split into two M/2-point
+// sub-FFTs sharing one M/2 exchange buffer, the accumulator in shared memory.)
 #define GRAF_CFG(M_, E_, S_)                                         \
   template <>                                                        \
   struct Cfg<M_> {                                                   \
     static constexpr int M = M_, E = E_, T = M_ / E_, S = S_;        \
     static constexpr int THREADS = T * S;                            \
-    static constexpr bool SPLIT = (M_ >= 16384);                     \
+    static constexpr bool SPLIT = (M_ >= 16384) && GRAF_SPLIT_16384;  \
     static constexpr int MX = SPLIT ? M_ / 2 : M_;  /* exchanged FFT length */ \
     static constexpr int XS = MX + MX / Pad<SPLIT ? E_ / 2 : E_>::P;  /* padded exchange */ \
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
-    static constexpr bool G_SMEM = true;                             \
+    static constexpr bool G_TMEM = (M_ >= 16384) && !SPLIT;          \
+    static constexpr bool G_SMEM = !G_TMEM;                          \
   };
 // Defaults; a tuning build may override one size with -DGRAF_E_<M>=.. -DGRAF_S_<M>=..
 #ifndef GRAF_E_64
@@ -409,6 +415,53 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// ---- tensor memory (TMEM) as a thread-private accumulator (G_TMEM, M = 16384).  A CTA
+// allocates 256 of the SM's 512 TMEM columns; warp w may touch lanes 32 (w % 4) .. +31,
+// so thread (w, lane) owns TMEM lane 32 (w % 4) + lane and the 64 columns 64 (w / 4) ..:
+// with 512 threads that is 16384 complex accumulators, one per time index n = t + e T.
+constexpr int kTmemCols = 256;
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {   // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(slot)),
+               "n"(kTmemCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {   // one full warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kTmemCols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// wait::ld that also ties the loaded registers to the wait, so no use of them can be
+// scheduled above it
+__device__ __forceinline__ void tmem_wait_ld16(float (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(r[0]), "+f"(r[1]), "+f"(r[2]), "+f"(r[3]), "+f"(r[4]), "+f"(r[5]), "+f"(r[6]), "+f"(r[7]),
+                 "+f"(r[8]), "+f"(r[9]), "+f"(r[10]), "+f"(r[11]), "+f"(r[12]), "+f"(r[13]), "+f"(r[14]), "+f"(r[15])
+               :
+               : "memory");
+}
+// 16 consecutive 32-bit columns of this thread's lane (8 complex accumulators)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),
+        "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]), "=f"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]), "f"(r[8]), "f"(r[9]),
+      "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]), "f"(r[15])
+      : "memory");
+}
+
 // slots per batch of predicated accumulator loads in the correlation (loads of a
 // batch are issued back to back, then the stores)
 #ifndef GRAF_CORR_CHUNK
@@ -591,6 +644,15 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     tw.tab1 = tab;
   }
   const float2 wt = SPLIT ? g_tw[t0 * (kMaxM / M)] : make_float2(1.f, 0.f);  // W_M^t (split stage)
+  // TMEM gradient accumulator (G_TMEM): warp 0 allocates, the address is read after the
+  // prologue barrier; thread (w, lane) owns lane 32 (w % 4) + lane, columns 64 (w / 4) ..
+  constexpr bool kTmem = GRAD && C::G_TMEM;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
+  if constexpr (kTmem) {
+    static_assert(THREADS == 512 && E == 32, "TMEM accumulator layout: 512 threads x 32 slots");
+    if (warp == 0) tmem_alloc(tslot);
+    tmem_fence_before();
+  }
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
   using Mask = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
   using VMask = Mask;
@@ -604,6 +666,17 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     mlb |= (Mask)(ad <= p.ml_d ? 1 : 0) << e;
   }
   __syncthreads();
+  uint32_t tacc = 0;   // this thread's TMEM accumulator address (lane field | column)
+  if constexpr (kTmem) {
+    tmem_fence_after();
+    tacc = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    float z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st16(tacc + 16 * c, z);
+    tmem_wait_st();
+  }
   const double Ed = red[0];
   // CROSS: normalisation by E1 E2 (reading R25); invE = 1/sqrt(E1 E2) for the surface
   const double Ed2 = CROSS ? red[1] : Ed;
@@ -719,6 +792,18 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           for (int e = 0; e < E / 2; ++e) v[e] = cmulc(a[e * T], c[e * T]);
 #pragma unroll
           for (int e = E / 2; e < E; ++e) v[e] = make_float2(0.f, 0.f);
+        } else if constexpr (!C::S_SMEM) {
+          // global s copy (M = 16384): slots outside the row's support load nothing (about
+          // half of a full-plane row); their lag products are exactly zero
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            float2 x = make_float2(0.f, 0.f), y = x;
+            if ((vmask >> e) & 1) {
+              x = a[e * T];
+              y = c[e * T];
+            }
+            v[e] = cmulc(x, y);
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < E; ++e) v[e] = cmulc(a[e * T], c[e * T]);
@@ -887,6 +972,54 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           tgp = tb0 + (size_t)(rowp < 0 ? 0 : rowp) * M;
           tgn = tb0 + (size_t)(rown < 0 ? 0 : rown) * M;
         }
+        // Full-plane centred single pass (R13; c5's loss), fast form.  The region is the whole
+        // plane minus the origin, so only slot 0 of thread 0 in row 0 is outside it.  When
+        // every u = (x - xbar)/T of this warp's row lies in (-1/8, 1/8) (c5: |u| < 0.11),
+        // expm1(u) = u (1 + u/2 + u^2/6 + u^3/24 + u^4/120) to < 5e-8 relative, with no MUFU
+        // and no selects; otherwise the general loop below runs.
+        // (T >= 32: a warp works on one row, so the vote below is warp-uniform; with T < 32
+        // the lanes of a warp hold different rows and some may skip this block)
+        bool fast_done = false;
+        if constexpr (KIND == K_PASS2 && !WGT && !CROSS && T >= 32) {
+          if (p.onepass) {
+            const bool in0 = !(k == 0 && t0 == 0);          // the origin cell (k, m) = (0, 0)
+            float mchi = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const float chi = fmaf(v[e].y, v[e].y, v[e].x * v[e].x);
+              mchi = fmaxf(mchi, (e == 0 && !in0) ? 0.f : chi);
+            }
+            const float cu = invE2 * p.invT, cb = -p.xbar * p.invT;
+            const bool ok = (-cb < 0.125f) && (fmaf(mchi, cu, cb) < 0.125f);
+            if (__all_sync(0xffffffffu, ok)) {
+              const float gl = p.lam_psl * gsc;
+              float sS = 0.f, sC = 0.f, sF = 0.f;
+#pragma unroll
+              for (int e = 0; e < E; ++e) {
+                const float chi = fmaf(v[e].y, v[e].y, v[e].x * v[e].x);
+                const float u = fmaf(chi, cu, cb);
+                const float q = fmaf(u, fmaf(u, fmaf(u, fmaf(u, 1.f / 120.f, 1.f / 24.f), 1.f / 6.f), 0.5f), 1.f);
+                float ec = u * q;
+                float ch = chi;
+                if (e == 0) {   // (compile-time slot: the origin test costs two selects per row)
+                  ec = in0 ? ec : 0.f;
+                  ch = in0 ? chi : 0.f;
+                }
+                sS += ch;
+                sC += ec;
+                sF = fmaf(ec, chi, sF);
+                const float sc = ec * gl;
+                v[e] = make_float2(v[e].x * sc, v[e].y * sc);
+              }
+              rowS = sS;
+              rowC1 = sC;
+              rowF = p.lam_psl * sF;
+              rowM1 = mchi * invE2;
+              fast_done = true;
+            }
+          }
+        }
+        if (!fast_done) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           if (eb && e != 0 && e != E - 1) continue;   // outside the band: no term, G unused
@@ -942,6 +1075,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             rowF = fmaf(fp, chi, rowF);
             v[e] = cscale(v[e], fp * gsc);
           }
+        }
         }
         if constexpr (KIND == K_ISL) rowF = p.lam_isl * rowS;
         accS += (double)(mult * rowS);
@@ -1016,7 +1150,47 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const int tb = SPLIT ? 2 * t : t;
         // predicated shared-memory read-modify-writes (no branches; an out-of-support
         // slot neither loads nor stores its accumulator)
-        if (p.periodic) {
+        if constexpr (kTmem) {
+          // Both terms accumulate at the thread's OWN positions p = t + eT, so the
+          // accumulator is thread-private (TMEM):
+          //   g[p] += H[k,p] s[p-k]             (p in the row's support [lo, hi))
+          //         + conj(H[k,p+k]) s[p+k]      (p+k in [lo, hi): the shifted H from smem)
+          // (periodic: every index mod N).  H goes through the exchange buffer once.
+          float2* hb = sh;
+#pragma unroll
+          for (int e = 0; e < E; ++e) hb[t + e * T] = v[e];
+          sync();
+          const bool per = p.periodic != 0;
+#pragma unroll
+          for (int c = 0; c < E / 8; ++c) {
+            float acc[16], d[16];
+            tmem_ld16(tacc + 16 * c, acc);   // in flight while this chunk's terms are formed
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int e = 8 * c + i;
+              const int pp = t + e * T;
+              const int q1 = per ? ((pp - k) & (N - 1)) : pp - k;            // s index, term 1
+              const int q2 = per ? ((pp + k) & (N - 1)) : pp + k;            // H and s index, term 2
+              const bool in1 = lrow && (per || (pp >= lo && pp < hi));
+              const bool in2 = lrow && (per || (q2 >= lo && q2 < hi));
+              float2 s1 = make_float2(0.f, 0.f), s2 = s1, h2 = s1;
+              if (in1) s1 = sv[q1];
+              if (in2) {
+                s2 = sv[q2];
+                h2 = hb[q2];
+              }
+              const float2 a1 = cmul(v[e], s1);
+              const float2 a2 = cmulc(s2, h2);      // conj(H) s
+              d[2 * i] = a1.x + a2.x;
+              d[2 * i + 1] = a1.y + a2.y;
+            }
+            tmem_wait_ld16(acc);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += d[i];
+            tmem_st16(tacc + 16 * c, acc);
+          }
+          tmem_wait_st();
+        } else if (p.periodic) {
           // circular lag products (M == N): every slot is in the support; term 1 reads
           // s[(n - k) mod N] from the periodic copy in s_pad, term 2 wraps its position.
           const int kc = k < 0 ? k + N : k;   // K_ADJ rows may be negative delays
@@ -1222,6 +1396,29 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     }
   }
 
+  // ---- TMEM accumulator -> this CTA's partial g (thread-private: no ordering question),
+  //      then the TMEM columns go back
+  if constexpr (kTmem) {
+    float2* gout = p.gpart + ((size_t)b * P + pb) * N;
+#pragma unroll
+    for (int c = 0; c < E / 8; ++c) {
+      float acc[16];
+      tmem_ld16(tacc + 16 * c, acc);
+      tmem_wait_ld16(acc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int n = t0 + (8 * c + i) * T;
+        if (n < N) gout[n] = make_float2(acc[2 * i], acc[2 * i + 1]);
+      }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc(*tslot);
+    }
+  }
+
   // ---- gradient accumulators of all slots -> this CTA's partial g (fixed slot order)
   if constexpr (GRAD && C::G_SMEM) {
     float2* gout = p.fuse ? gacc_sh + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
@@ -1245,7 +1442,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   }
 
   // ---- fused finalize over the cluster (SURVEY §8(a) a4 + a7 final, K5)
-  if constexpr (KIND == K_ISL) {
+  if constexpr (KIND == K_ISL && C::G_SMEM) {
     if (p.fuse) {
       namespace cg = cooperative_groups;
       cg::cluster_group cl = cg::this_cluster();

@@ -154,7 +154,7 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
     pl.fixedP = true;   // later passes of the same call reuse it
   }
   rp.fuse = 0;
-  if (KIND == K_ISL && !CROSS && pl.fuse_req && pl.P >= 2 && pl.P <= 8) {   // (P = 1: measured slower as a cluster launch)
+  if (KIND == K_ISL && !CROSS && Cfg<M>::G_SMEM && pl.fuse_req && pl.P >= 2 && pl.P <= 8) {   // (P = 1: measured slower as a cluster launch)
     rp.fuse = 1;
     pl.fused = true;
   }

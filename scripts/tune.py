@@ -30,7 +30,7 @@ def build(cfg, specs):
         out = os.path.join(VDIR, f"libgraf_c{cfg}_{tag}.so")
         try:
             _build.compile_link(out, srcs, defines=[f"GRAF_ONLY_M={M}"] + [d for d in defs.split(",") if d],
-                                objdir=os.path.join(ROOT, "build", "variants", "obj_" + tag))
+                                objdir=os.path.join("/tmp/graf_build", "variants", "obj_" + tag))
             print(tag, "rc 0")
         except Exception as e:   # noqa: BLE001
             print(tag, "failed", e)
@@ -95,7 +95,7 @@ def run(cfg):
     libs = sorted(f for f in os.listdir(VDIR) if f.startswith(f"libgraf_c{cfg}_"))
     base = os.path.join(ROOT, "paper_2506_22935_b200", "libgraf.so")
     for lib in [base] + [os.path.join(VDIR, f) for f in libs]:
-        r = subprocess.run([sys.executable, __file__, "one", lib, str(cfg)], capture_output=True, text=True)
+        r = subprocess.run([sys.executable, __file__, "one", lib, str(cfg)], capture_output=True, text=True, timeout=300)
         print(r.stdout.strip() or r.stderr.strip()[-400:], flush=True)
 
 
