@@ -536,7 +536,7 @@ graf_status run_finalize(const graf_af_desc* af, const graf_loss_desc* L, const 
       fc.grad2 = f.grad2 ? f.grad2 + b0 * af->n : nullptr;
     }
     fc.B = (int)nb;
-    finalize_kernel<<<(unsigned)nb, 256, 0, st>>>(fc);
+    finalize_kernel<<<dim3((unsigned)nb, (unsigned)((af->n + kFinChunk - 1) / kFinChunk)), 256, 0, st>>>(fc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "finalize_kernel launch");
     ++t_launches;

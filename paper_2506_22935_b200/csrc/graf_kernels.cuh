@@ -992,7 +992,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             const float cu = invE2 * p.invT, cb = -p.xbar * p.invT;
             const bool ok = (-cb < 0.125f) && (fmaf(mchi, cu, cb) < 0.125f);
             if (__all_sync(0xffffffffu, ok)) {
+#ifdef GRAF_MUTATE_NO_PSL   // mutation check only: drop the soft-PSL term of f'
+              const float gl = 0.f;
+#else
               const float gl = p.lam_psl * gsc;
+#endif
               float sS = 0.f, sC = 0.f, sF = 0.f;
 #pragma unroll
               for (int e = 0; e < E; ++e) {
@@ -1066,10 +1070,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             if (use_centred) {
               const float ec = expm1_fast((x - p.xbar) * p.invT);
               fp = p.lam_psl * (ec - ebar) * invZc;
+#ifdef GRAF_MUTATE_NO_PSL
+              fp = 0.f;
+#endif
               rowC1 += in ? ec : 0.f;                      // (single pass: Z_c and the validity max)
               rowM1 = fmaxf(rowM1, in ? x : -INFINITY);
             } else {
               fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
+#ifdef GRAF_MUTATE_NO_PSL
+              fp = p.lam_isl * w;
+#endif
             }
             fp = in ? fp : 0.f;
             rowF = fmaf(fp, chi, rowF);
@@ -1589,6 +1599,8 @@ struct FinalizeParams {
   const int32_t* skip;   // skipped waveforms: outputs left untouched
 };
 
+constexpr int kFinChunk = 1024;   // gradient positions per finalize CTA (grid.y)
+
 __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   const int b = blockIdx.x;
   if (f.skip && f.skip[b]) return;
@@ -1597,6 +1609,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   const float2* sg2 = f.s2 ? f.s2 + (size_t)b * N : nullptr;
   __shared__ double sh[4];
   const bool one = f.one && f.one[b].reserved == 1.0;   // single-pass soft-PSL result is valid
+  // grid.y splits the gradient's N positions over CTAs (c5: 8 waveforms would otherwise be
+  // 8 CTAs summing 16384 x P partials each); every CTA recomputes the O(N) scalars, and
+  // only chunk 0 writes the loss
+  const int n0 = blockIdx.y * kFinChunk, n1 = min(N, n0 + kFinChunk);
+  double* const loss_out = blockIdx.y == 0 ? f.loss : nullptr;
   if (threadIdx.x < 32) {
     const double e = warp_energy(sg, N, threadIdx.x);
     // cross-ambiguity: E1 E2 replaces E^2 (reading R25)
@@ -1620,13 +1637,16 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
         // is scaled by 1/Z_c; LSE = xbar + T log Z_c (reading R13)
         const double zc = f.omega + f.one[b].cen_sum;
         sh[3] = 1.0 / zc;
+#ifdef GRAF_MUTATE_NO_ZC   // mutation check only: drop the 1/Z_c scale of the single pass
+        sh[3] = 1.0;
+#endif
         const double Sg = f.sp ? f.global[b].isl_sum : S;
-        if (f.loss)
-          f.loss[b] = f.lam_isl * (f.normalize ? Sg / (e * e2) : Sg) + f.lam_psl * ((double)f.xbar + (double)f.T * log(zc));
+        if (loss_out)
+          loss_out[b] = f.lam_isl * (f.normalize ? Sg / (e * e2) : Sg) + f.lam_psl * ((double)f.xbar + (double)f.T * log(zc));
       } else if (f.sp) {
         sh[3] = 0.0;   // invalid global single pass: the caller recomputes with two passes
-        if (f.loss) f.loss[b] = __longlong_as_double(0x7ff8000000000000ll);
-      } else if (f.loss) {
+        if (loss_out) loss_out[b] = __longlong_as_double(0x7ff8000000000000ll);
+      } else if (loss_out) {
         double Sg = S, mg = m, Zg = Z;
         if (f.global) {
           Sg = f.global[b].isl_sum;
@@ -1636,7 +1656,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
         double L = f.lam_isl * (f.normalize ? Sg / (e * e2) : Sg);
         if (f.lam_psl != 0.f) L += f.lam_psl * (mg + (double)f.T * log(Zg));
         if (f.lam_match != 0.f) L += f.lam_match * Mt;
-        f.loss[b] = L;
+        loss_out[b] = L;
       }
     }
   }
@@ -1649,10 +1669,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalizeParams f) {
   const float coef = nt ? (float)((sg2 ? 1.0 : 2.0) * sh[1] * gs / (E * E * E2)) : 0.f;
   const float coef2 = nt ? (float)(sh[1] / (E * E2 * E2)) : 0.f;
   if (f.sp && !one) {   // invalid sharded single pass: the unscaled sums may hold inf (expm1 overflow)
-    for (int n = threadIdx.x; n < N; n += blockDim.x) f.grad[(size_t)b * N + n] = make_float2(0.f, 0.f);
+    for (int n = n0 + threadIdx.x; n < n1; n += blockDim.x) f.grad[(size_t)b * N + n] = make_float2(0.f, 0.f);
     return;
   }
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+  for (int n = n0 + threadIdx.x; n < n1; n += blockDim.x) {
     double gx = 0, gy = 0;
     for (int q = 0; q < f.P; ++q) {
       const float2 a = f.gpart[((size_t)b * f.P + q) * N + n];
