@@ -116,14 +116,14 @@ cudaError_t ensure_twiddles(cudaStream_t st) {
 
 struct CfgInfo {
   int M, E, T, S, threads, XS, tab1;
-  bool s_smem, g_smem;
+  bool s_smem, g_smem, s_trim;
 };
 
 template <int M>
 CfgInfo cfg_info() {
   using C = Cfg<M>;
   constexpr int E2 = C::SPLIT ? C::E / 2 : C::E;
-  return CfgInfo{M, C::E, C::T, C::S, C::THREADS, C::XS, Twiddles<C::MX, E2>::TAB1, C::S_SMEM, C::G_SMEM};
+  return CfgInfo{M, C::E, C::T, C::S, C::THREADS, C::XS, Twiddles<C::MX, E2>::TAB1, C::S_SMEM, C::G_SMEM, C::S_TRIM};
 }
 
 bool cfg_for(int M, CfgInfo* ci) {
@@ -291,7 +291,10 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
     }
   }
   const size_t nsig = cross ? 2 : 1;   // staged waveforms and gradient accumulator sets
-  pl.smem = sizeof(float2) * (64 + (ci.s_smem ? ((N + af->m + 1) & ~1) : 0) +
+  // staged s: [N zeros][N samples][M - N zeros], or unpadded (s_trim: [N] / periodic [2N])
+  const size_t s_elems = !ci.s_smem ? 0 : ci.s_trim ? (size_t)(((af->periodic ? 2 * N : N) + 1) & ~1)
+                                                    : (size_t)((N + af->m + 1) & ~1);
+  pl.smem = sizeof(float2) * (64 + s_elems +
                               (cross ? (size_t)((2 * N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
                               (grad && ci.g_smem ? nsig * ci.S * N : 0) + (size_t)ci.tab1);
   if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512 && !af->periodic && !cross) {

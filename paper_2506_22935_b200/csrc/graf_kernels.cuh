@@ -105,6 +105,13 @@ struct Cfg;
 #ifndef GRAF_SPLIT_16384
 #define GRAF_SPLIT_16384 0   // 1 = round-1 A/B build: the radix-2 split with the smem accumulator
 #endif
+#ifndef GRAF_TMEM_8192
+#define GRAF_TMEM_8192 1     // 0 = round-1 A/B build for M = 8192 (padded s, smem accumulator)
+#endif
+#define GRAF_TMEM_8192_OK(M_) ((M_) != 8192 || GRAF_TMEM_8192)
+#ifndef GRAF_MINB_8192
+#define GRAF_MINB_8192 2     // M = 8192 with the trimmed s: two resident CTAs per SM (64 registers)
+#endif
 // E = values per thread, T = threads per row slot, S = row slots per CTA.
 // M = 16384: one 16384-point Stockham FFT per row (E = 32, passes 32 x 32 x 16, a 132 KiB
 // exchange buffer) with the gradient accumulator in TENSOR MEMORY (G_TMEM: 128 KiB of the
@@ -120,7 +127,10 @@ struct Cfg;
     static constexpr int MX = SPLIT ? M_ / 2 : M_;  /* exchanged FFT length */ \
     static constexpr int XS = MX + MX / Pad<SPLIT ? E_ / 2 : E_>::P;  /* padded exchange */ \
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
-    static constexpr bool G_TMEM = (M_ >= 16384) && !SPLIT;          \
+    static constexpr bool G_TMEM = (M_ >= 8192) && !SPLIT && GRAF_TMEM_8192_OK(M_); \
+    /* M = 8192: s staged WITHOUT zero padding (aperiodic: [N samples]; every read of it is \
+       predicated to the row's support), so two CTAs fit an SM beside the exchange buffer */ \
+    static constexpr bool S_TRIM = (M_ == 8192) && G_TMEM;           \
     static constexpr bool G_SMEM = !G_TMEM;                          \
   };
 // Defaults; a tuning build may override one size with -DGRAF_E_<M>=.. -DGRAF_S_<M>=..
@@ -339,7 +349,8 @@ struct MinBlocks {
 #ifdef GRAF_MINB
   static constexpr int value = GRAF_MINB;
 #else
-  static constexpr int value = M <= 16 ? 2 : M == 1024 ? ((KIND == 0 || KIND == 4) ? 3 : 2) : M <= 1024 ? 4 : M <= 4096 ? 2 : 1;
+  static constexpr int value = M <= 16 ? 2 : M == 1024 ? ((KIND == 0 || KIND == 4) ? 3 : 2) : M <= 1024 ? 4 : M <= 4096 ? 2
+                              : (M == 8192 && GRAF_TMEM_8192) ? GRAF_MINB_8192 : 1;
 #endif
 };
 // radix-2 split stage between the two M/2-point halves (twiddle W_M^{t + e T} =
@@ -419,16 +430,18 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // allocates 256 of the SM's 512 TMEM columns; warp w may touch lanes 32 (w % 4) .. +31,
 // so thread (w, lane) owns TMEM lane 32 (w % 4) + lane and the 64 columns 64 (w / 4) ..:
 // with 512 threads that is 16384 complex accumulators, one per time index n = t + e T.
-constexpr int kTmemCols = 256;
+// (M = 8192, E = 16: 128 columns per CTA, so two CTAs share an SM's TMEM)
+template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot) {   // one full warp
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    (unsigned)__cvta_generic_to_shared(slot)),
-               "n"(kTmemCols)
+               "n"(NCOLS)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
+template <int NCOLS>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {   // one full warp
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kTmemCols) : "memory");
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
 }
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -562,7 +575,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // lag product and the correlation read s[n-k] with no bounds arithmetic.
   double* red = reinterpret_cast<double*>(smem);
   float2* s_pad = smem + 64;
-  const int NP2 = (N + M + 1) & ~1;
+  const int NP2 = C::S_TRIM ? (((p.periodic ? 2 * N : N) + 1) & ~1) : ((N + M + 1) & ~1);
   // CROSS: the second waveform, zero-padded over [-N, M + N): unfolded rows k < 0 read
   // s2[n - k] for every slot n < M (s[n] = 0 beyond N, but 0 * garbage may be NaN)
   float2* s2_pad = s_pad + (C::S_SMEM ? NP2 : 0);
@@ -574,7 +587,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // 2 extra keep s[N-1] inside the row of the shifted copy when N == M
   const int NL = N + (N & 1);
   const size_t RP = (size_t)(NL + M + 2);
-  const float2* sv = C::S_SMEM ? s_pad + N : p.s_pad + (size_t)b * RP + NL;
+  // (S_TRIM: aperiodic [N samples], periodic [N-sample copy][N samples])
+  const float2* sv = C::S_SMEM ? s_pad + ((C::S_TRIM && !p.periodic) ? 0 : N) : p.s_pad + (size_t)b * RP + NL;
   // zero-padded Doppler axis (2N <= M, aperiodic): time slots e >= E/2 hold n >= M/2 >= N
   // (compiled for M >= 2048 only: the extra code path measured 3 % slower at M = 1024)
   constexpr bool kHalfSizes = (M >= 2048) && !SPLIT;
@@ -606,7 +620,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
                (size_t)slot * p.stg_floats;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
-  if constexpr (C::S_SMEM) {
+  if constexpr (C::S_TRIM) {
+    const int n_st = p.periodic ? 2 * N : N;
+    for (int i = threadIdx.x; i < n_st; i += THREADS) s_pad[i] = sg[i >= N ? i - N : i];
+  } else if constexpr (C::S_SMEM) {
     for (int i = threadIdx.x; i < N + M; i += THREADS)
       // aperiodic: N zeros on the left; periodic: a copy of s, so s_pad[n - k] = s[(n - k) mod N]
       s_pad[i] = (i < 2 * N && (i >= N || p.periodic)) ? sg[i >= N ? i - N : i] : make_float2(0.f, 0.f);
@@ -649,8 +666,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   constexpr bool kTmem = GRAD && C::G_TMEM;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
   if constexpr (kTmem) {
-    static_assert(THREADS == 512 && E == 32, "TMEM accumulator layout: 512 threads x 32 slots");
-    if (warp == 0) tmem_alloc(tslot);
+    static_assert(THREADS == 512 && (E == 32 || E == 16), "TMEM accumulator layout: 512 threads x E slots");
+    if (warp == 0) tmem_alloc<8 * E>(tslot);
     tmem_fence_before();
   }
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
@@ -669,12 +686,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   uint32_t tacc = 0;   // this thread's TMEM accumulator address (lane field | column)
   if constexpr (kTmem) {
     tmem_fence_after();
-    tacc = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    tacc = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(2 * E * (warp >> 2));
     float z[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) z[i] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_st16(tacc + 16 * c, z);
+    for (int c = 0; c < E / 8; ++c) tmem_st16(tacc + 16 * c, z);
     tmem_wait_st();
   }
   const double Ed = red[0];
@@ -789,12 +806,23 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         if (kHalfSizes && half) {
           // zero-padded row (2N <= M): the samples n = t + eT >= M/2 >= N are zero
 #pragma unroll
-          for (int e = 0; e < E / 2; ++e) v[e] = cmulc(a[e * T], c[e * T]);
+          for (int e = 0; e < E / 2; ++e) {
+            if constexpr (C::S_TRIM) {   // unpadded s: loads only inside the row's support
+              float2 x = make_float2(0.f, 0.f), y = x;
+              if ((vmask >> e) & 1) {
+                x = a[e * T];
+                y = c[e * T];
+              }
+              v[e] = cmulc(x, y);
+            } else {
+              v[e] = cmulc(a[e * T], c[e * T]);
+            }
+          }
 #pragma unroll
           for (int e = E / 2; e < E; ++e) v[e] = make_float2(0.f, 0.f);
-        } else if constexpr (!C::S_SMEM) {
-          // global s copy (M = 16384): slots outside the row's support load nothing (about
-          // half of a full-plane row); their lag products are exactly zero
+        } else if constexpr (!C::S_SMEM || C::S_TRIM) {
+          // global s copy (M = 16384) or the unpadded smem copy (M = 8192): slots outside the
+          // row's support load nothing; their lag products are exactly zero
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             float2 x = make_float2(0.f, 0.f), y = x;
@@ -1166,13 +1194,18 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           //   g[p] += H[k,p] s[p-k]             (p in the row's support [lo, hi))
           //         + conj(H[k,p+k]) s[p+k]      (p+k in [lo, hi): the shifted H from smem)
           // (periodic: every index mod N).  H goes through the exchange buffer once.
+          // (a zero-padded row, 2N <= M: positions n >= M/2 >= N carry no support, so only
+          // the lower half of the slots writes H or touches its accumulators)
           float2* hb = sh;
+          const int nch = (kHalfSizes && half) ? E / 16 : E / 8;
 #pragma unroll
-          for (int e = 0; e < E; ++e) hb[t + e * T] = v[e];
+          for (int e = 0; e < E; ++e)
+            if (8 * nch > e) hb[t + e * T] = v[e];
           sync();
           const bool per = p.periodic != 0;
 #pragma unroll
           for (int c = 0; c < E / 8; ++c) {
+            if (c >= nch) break;
             float acc[16], d[16];
             tmem_ld16(tacc + 16 * c, acc);   // in flight while this chunk's terms are formed
 #pragma unroll
@@ -1425,7 +1458,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     __syncthreads();
     if (warp == 0) {
       tmem_fence_after();
-      tmem_dealloc(*tslot);
+      tmem_dealloc<8 * E>(*tslot);
     }
   }
 
