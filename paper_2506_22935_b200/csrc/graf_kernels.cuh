@@ -664,10 +664,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // TMEM gradient accumulator (G_TMEM): warp 0 allocates, the address is read after the
   // prologue barrier; thread (w, lane) owns lane 32 (w % 4) + lane, columns 64 (w / 4) ..
   constexpr bool kTmem = GRAD && C::G_TMEM;
+  // columns: THREADS / 128 warps per lane quarter, 2E columns (E complex) per thread
+  constexpr int kTmemNC = 2 * E * (THREADS / 128);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
   if constexpr (kTmem) {
-    static_assert(THREADS == 512 && (E == 32 || E == 16), "TMEM accumulator layout: 512 threads x E slots");
-    if (warp == 0) tmem_alloc<8 * E>(tslot);
+    static_assert(THREADS % 128 == 0 && (E % 8) == 0, "TMEM accumulator layout: whole lane quarters");
+    static_assert(kTmemNC == 32 || kTmemNC == 64 || kTmemNC == 128 || kTmemNC == 256 || kTmemNC == 512,
+                  "TMEM allocation: a power of two >= 32 columns");
+    if (warp == 0) tmem_alloc<kTmemNC>(tslot);
     tmem_fence_before();
   }
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
@@ -1458,7 +1462,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     __syncthreads();
     if (warp == 0) {
       tmem_fence_after();
-      tmem_dealloc<8 * E>(*tslot);
+      tmem_dealloc<kTmemNC>(*tslot);
     }
   }
 
