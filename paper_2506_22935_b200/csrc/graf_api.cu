@@ -292,11 +292,13 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   }
   const size_t nsig = cross ? 2 : 1;   // staged waveforms and gradient accumulator sets
   // staged s: [N zeros][N samples][M - N zeros], or unpadded (s_trim: [N] / periodic [2N])
-  const size_t s_elems = !ci.s_smem ? 0 : ci.s_trim ? (size_t)(((af->periodic ? 2 * N : N) + 1) & ~1)
-                                                    : (size_t)((N + af->m + 1) & ~1);
+  // (cross-ambiguity kernels keep the padded s and shared-memory accumulators, graf_kernels.cuh)
+  const bool s_trim = ci.s_trim && !cross, g_smem = ci.g_smem || cross;
+  const size_t s_elems = !ci.s_smem ? 0 : s_trim ? (size_t)(((af->periodic ? 2 * N : N) + 1) & ~1)
+                                                 : (size_t)((N + af->m + 1) & ~1);
   pl.smem = sizeof(float2) * (64 + s_elems +
                               (cross ? (size_t)((2 * N + af->m + 1) & ~1) : 0) + (size_t)ci.S * ci.XS +
-                              (grad && ci.g_smem ? nsig * ci.S * N : 0) + (size_t)ci.tab1);
+                              (grad && g_smem ? nsig * ci.S * N : 0) + (size_t)ci.tab1);
   if (kind == Kind::LossGrad && af->n == af->m && ci.g_smem && af->m <= 512 && !af->periodic && !cross) {
     pl.gpad_ok = true;
     pl.smem_gpad = sizeof(float2) * (size_t)ci.S * N;

@@ -109,6 +109,12 @@ struct Cfg;
 #define GRAF_TMEM_8192 1     // 0 = round-1 A/B build for M = 8192 (padded s, smem accumulator)
 #endif
 #define GRAF_TMEM_8192_OK(M_) ((M_) != 8192 || GRAF_TMEM_8192)
+#ifndef GRAF_TMEM_1024
+#define GRAF_TMEM_1024 0     // 1: M = 1024 with TMEM accumulators + unpadded s (measured slower for c3: profiles/r02/tune_c3_ab.txt)
+#endif
+#ifndef GRAF_MINB_1024G
+#define GRAF_MINB_1024G 4    // resident CTAs per SM of the M = 1024 gradient kernels with GRAF_TMEM_1024
+#endif
 #ifndef GRAF_MINB_8192
 #define GRAF_MINB_8192 2     // M = 8192 with the trimmed s: two resident CTAs per SM (64 registers)
 #endif
@@ -127,10 +133,11 @@ struct Cfg;
     static constexpr int MX = SPLIT ? M_ / 2 : M_;  /* exchanged FFT length */ \
     static constexpr int XS = MX + MX / Pad<SPLIT ? E_ / 2 : E_>::P;  /* padded exchange */ \
     static constexpr bool S_SMEM = (M_ <= 8192);                     \
-    static constexpr bool G_TMEM = (M_ >= 8192) && !SPLIT && GRAF_TMEM_8192_OK(M_); \
+    static constexpr bool G_TMEM = ((M_ >= 8192) && !SPLIT && GRAF_TMEM_8192_OK(M_)) || \
+                                   ((M_ == 1024) && GRAF_TMEM_1024);                  \
     /* M = 8192: s staged WITHOUT zero padding (aperiodic: [N samples]; every read of it is \
        predicated to the row's support), so two CTAs fit an SM beside the exchange buffer */ \
-    static constexpr bool S_TRIM = (M_ == 8192) && G_TMEM;           \
+    static constexpr bool S_TRIM = (M_ == 8192 || M_ == 1024) && G_TMEM; \
     static constexpr bool G_SMEM = !G_TMEM;                          \
   };
 // Defaults; a tuning build may override one size with -DGRAF_E_<M>=.. -DGRAF_S_<M>=..
@@ -349,7 +356,8 @@ struct MinBlocks {
 #ifdef GRAF_MINB
   static constexpr int value = GRAF_MINB;
 #else
-  static constexpr int value = M <= 16 ? 2 : M == 1024 ? ((KIND == 0 || KIND == 4) ? 3 : 2) : M <= 1024 ? 4 : M <= 4096 ? 2
+  static constexpr int value = M <= 16 ? 2 : M == 1024 ? ((KIND == 0 || KIND == 4) ? 3 : GRAF_TMEM_1024 ? GRAF_MINB_1024G : 2)
+                              : M <= 1024 ? 4 : M <= 4096 ? 2
                               : (M == 8192 && GRAF_TMEM_8192) ? GRAF_MINB_8192 : 1;
 #endif
 };
@@ -552,6 +560,9 @@ __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi
 template <int M, int KIND, bool WGT, bool CROSS = false>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
+  // cross-ambiguity kernels keep the padded s and the shared-memory accumulators
+  // (two accumulator sets and unfolded rows): the TMEM / unpadded layouts are auto only
+  constexpr bool kGtmem = C::G_TMEM && !CROSS, kGsmem = !kGtmem, kStrim = C::S_TRIM && !CROSS;
   constexpr int E = C::E, T = C::T, S = C::S, THREADS = C::THREADS, XS = C::XS;
   constexpr int LT = ilog2(T);
   constexpr bool FWD = (KIND == K_FWD || KIND == K_FWDA);
@@ -575,7 +586,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // lag product and the correlation read s[n-k] with no bounds arithmetic.
   double* red = reinterpret_cast<double*>(smem);
   float2* s_pad = smem + 64;
-  const int NP2 = C::S_TRIM ? (((p.periodic ? 2 * N : N) + 1) & ~1) : ((N + M + 1) & ~1);
+  const int NP2 = kStrim ? (((p.periodic ? 2 * N : N) + 1) & ~1) : ((N + M + 1) & ~1);
   // CROSS: the second waveform, zero-padded over [-N, M + N): unfolded rows k < 0 read
   // s2[n - k] for every slot n < M (s[n] = 0 beyond N, but 0 * garbage may be NaN)
   float2* s2_pad = s_pad + (C::S_SMEM ? NP2 : 0);
@@ -588,7 +599,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const int NL = N + (N & 1);
   const size_t RP = (size_t)(NL + M + 2);
   // (S_TRIM: aperiodic [N samples], periodic [N-sample copy][N samples])
-  const float2* sv = C::S_SMEM ? s_pad + ((C::S_TRIM && !p.periodic) ? 0 : N) : p.s_pad + (size_t)b * RP + NL;
+  const float2* sv = C::S_SMEM ? s_pad + ((kStrim && !p.periodic) ? 0 : N) : p.s_pad + (size_t)b * RP + NL;
   // zero-padded Doppler axis (2N <= M, aperiodic): time slots e >= E/2 hold n >= M/2 >= N
   // (compiled for M >= 2048 only: the extra code path measured 3 % slower at M = 1024)
   constexpr bool kHalfSizes = (M >= 2048) && !SPLIT;
@@ -611,16 +622,16 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // beside the resident CTAs the gradient kernels need)
   constexpr bool kGpadSizes = (M <= 512);
   const int GS = p.gpad ? 2 * N : N;
-  float2* gacc = C::G_SMEM ? gacc_sh + (size_t)slot * GS + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
+  float2* gacc = kGsmem ? gacc_sh + (size_t)slot * GS + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
   constexpr int NG = CROSS ? 2 : 1;                           // accumulator sets (CROSS: g1, g2)
   float2* gacc2 = gacc + (size_t)S * GS;                      // CROSS: dL/ds2* accumulators
   // surface staging (bulk path): after the gradient accumulators, 16-byte aligned
   float* stg = reinterpret_cast<float*>(
-                   xch + (((size_t)S * XS + (GRAD && C::G_SMEM ? (size_t)NG * S * GS : 0) + 1) & ~(size_t)1)) +
+                   xch + (((size_t)S * XS + (GRAD && kGsmem ? (size_t)NG * S * GS : 0) + 1) & ~(size_t)1)) +
                (size_t)slot * p.stg_floats;
 
   // ---- a0: stage s, zero the gradient accumulators, energy
-  if constexpr (C::S_TRIM) {
+  if constexpr (kStrim) {
     const int n_st = p.periodic ? 2 * N : N;
     for (int i = threadIdx.x; i < n_st; i += THREADS) s_pad[i] = sg[i >= N ? i - N : i];
   } else if constexpr (C::S_SMEM) {
@@ -634,7 +645,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     }
   }
   if constexpr (GRAD) {
-    if constexpr (C::G_SMEM) {
+    if constexpr (kGsmem) {
       for (int i = threadIdx.x; i < NG * S * GS; i += THREADS) gacc_sh[i] = make_float2(0.f, 0.f);
     } else {
       for (int i = threadIdx.x; i < N; i += THREADS) gacc[i] = make_float2(0.f, 0.f);
@@ -663,7 +674,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const float2 wt = SPLIT ? g_tw[t0 * (kMaxM / M)] : make_float2(1.f, 0.f);  // W_M^t (split stage)
   // TMEM gradient accumulator (G_TMEM): warp 0 allocates, the address is read after the
   // prologue barrier; thread (w, lane) owns lane 32 (w % 4) + lane, columns 64 (w / 4) ..
-  constexpr bool kTmem = GRAD && C::G_TMEM;
+  constexpr bool kTmem = GRAD && kGtmem;
   // columns: THREADS / 128 warps per lane quarter, 2E columns (E complex) per thread
   constexpr int kTmemNC = 2 * E * (THREADS / 128);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
@@ -811,7 +822,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           // zero-padded row (2N <= M): the samples n = t + eT >= M/2 >= N are zero
 #pragma unroll
           for (int e = 0; e < E / 2; ++e) {
-            if constexpr (C::S_TRIM) {   // unpadded s: loads only inside the row's support
+            if constexpr (kStrim) {   // unpadded s: loads only inside the row's support
               float2 x = make_float2(0.f, 0.f), y = x;
               if ((vmask >> e) & 1) {
                 x = a[e * T];
@@ -824,7 +835,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
 #pragma unroll
           for (int e = E / 2; e < E; ++e) v[e] = make_float2(0.f, 0.f);
-        } else if constexpr (!C::S_SMEM || C::S_TRIM) {
+        } else if constexpr (!C::S_SMEM || kStrim) {
           // global s copy (M = 16384) or the unpadded smem copy (M = 8192): slots outside the
           // row's support load nothing; their lag products are exactly zero
 #pragma unroll
@@ -1447,6 +1458,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   //      then the TMEM columns go back
   if constexpr (kTmem) {
     float2* gout = p.gpart + ((size_t)b * P + pb) * N;
+    // one row slot: the thread's columns ARE the CTA's partial gradient; several slots (M =
+    // 1024: four rows per CTA, a warp each): every slot's columns go to the free exchange
+    // space as [slot][N], then a fixed-order sum over the slots (deterministic)
+    float2* gb = S == 1 ? gout : xch + (size_t)slot * N;
 #pragma unroll
     for (int c = 0; c < E / 8; ++c) {
       float acc[16];
@@ -1455,7 +1470,17 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int n = t0 + (8 * c + i) * T;
-        if (n < N) gout[n] = make_float2(acc[2 * i], acc[2 * i + 1]);
+        if (n < N) gb[n] = make_float2(acc[2 * i], acc[2 * i + 1]);
+      }
+    }
+    if constexpr (S > 1) {
+      static_assert(S == 1 || XS >= 1, "");
+      __syncthreads();
+      for (int n = threadIdx.x; n < N; n += THREADS) {
+        float2 a = xch[n];
+#pragma unroll 1
+        for (int sl = 1; sl < S; ++sl) a = cadd(a, xch[(size_t)sl * N + n]);
+        gout[n] = a;
       }
     }
     tmem_fence_before();
@@ -1467,7 +1492,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   }
 
   // ---- gradient accumulators of all slots -> this CTA's partial g (fixed slot order)
-  if constexpr (GRAD && C::G_SMEM) {
+  if constexpr (GRAD && kGsmem) {
     float2* gout = p.fuse ? gacc_sh + (p.gpad ? N : 0) : p.gpart + ((size_t)b * P + pb) * N;
     for (int n = threadIdx.x; n < N; n += THREADS) {
       const float2* g0 = gacc_sh + (p.gpad ? N : 0) + n;
@@ -1489,7 +1514,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   }
 
   // ---- fused finalize over the cluster (SURVEY §8(a) a4 + a7 final, K5)
-  if constexpr (KIND == K_ISL && C::G_SMEM) {
+  if constexpr (KIND == K_ISL && kGsmem) {
     if (p.fuse) {
       namespace cg = cooperative_groups;
       cg::cluster_group cl = cg::this_cluster();
