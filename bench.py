@@ -412,9 +412,17 @@ def run_graf(args, w, world):
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks (tests/test_gpu_bench_multirank.py): the multi-rank path exercised on ONE GPU
+    # with gloo collectives; the driver's runs use NCCL, one GPU per rank
+    backend = os.environ.get("GRAF_BENCH_DIST_BACKEND", "nccl")
+    if os.environ.get("GRAF_BENCH_ONE_GPU"):
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     W = max(3, args.warmup)

@@ -11,6 +11,8 @@ import torch
 from graf_inputs import SplitMix64, complex_gaussian, frank, random_phase
 from oracle import graf_oracle as O
 
+from gradtol import grad_tol
+
 pytestmark = pytest.mark.gpu
 
 graf = pytest.importorskip("paper_2506_22935_b200")
@@ -108,7 +110,7 @@ def check(s, spec_d, **kw):
     for b in range(s.shape[0]):
         L_ref, g_ref, t = O.loss_and_grad(s[b], N, ospec, periodic=True)
         assert abs(loss[b] - L_ref) <= 1e-4 * abs(L_ref), (b, loss[b], L_ref)
-        tol = 1e-4 * max(np.abs(g_ref).max(), t["sigma_g"])
+        tol = grad_tol(g_ref, t["sigma_g"])
         assert np.abs(g[b] - g_ref).max() <= tol, (b, np.abs(g[b] - g_ref).max(), tol)
     return loss, g, surf
 
