@@ -404,6 +404,12 @@ void fill_loss(RowParams& rp, const graf_af_desc* af, const graf_loss_desc* L) {
   // reading R13: constant-sum region -> centred soft-PSL weights
   const bool full = rp.kloss == (af->periodic ? N / 2 : N - 1) && L->d_max >= M / 2 && L->ml_k == 0 && L->ml_d == 0;
   rp.centred = (L->normalize && !L->w_k && !L->w_d && full && L->lambda_psl != 0.f) ? 1 : 0;
+  rp.const_sum = (L->normalize && !L->w_k && !L->w_d && full && af->m >= af->n) ? 1 : 0;
+  // whole delay / Doppler extent with a mainlobe block cut out: the complement form of the
+  // ISL gradient (kernels: f' = -lambda_isl on the block only)
+  const bool full_extent = rp.kloss == (af->periodic ? N / 2 : N - 1) && L->d_max >= M / 2;
+  rp.complement = (L->normalize && !L->w_k && !L->w_d && full_extent && af->m >= af->n && !rp.const_sum &&
+                   L->lambda_match == 0.f) ? 1 : 0;
   rp.omega = (double)(af->periodic ? N : 2 * N - 1) * M - 1.0;   // |Omega| of the full plane
   rp.want_argmax = L->lambda_hpsl != 0.f ? 1 : 0;
   rp.lam_match = L->lambda_match;

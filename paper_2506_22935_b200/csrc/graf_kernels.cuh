@@ -52,6 +52,14 @@ struct RowParams {
   int normalize;
   int shard_index, shard_count;
   int centred;
+  int const_sum;       // the region is constant-sum (full plane, normalised, unweighted, M >= N):
+                       // the ISL term's gradient is identically zero (volume identity), so pass 2
+                       // leaves it out instead of cancelling O(1) terms in fp32 (reading R13 (iii))
+  // the region spans the whole plane except a mainlobe block (normalised, unweighted, M >= N):
+  // the ISL over the whole plane is constant (volume identity), so the ISL gradient equals
+  // MINUS that of the excluded cells; the kernels give f' = -lambda_isl to the excluded cells
+  // and nothing to the region, instead of summing O(1) terms that cancel (round 2)
+  int complement;
   float xbar;
   double omega;        // |Omega| (full region, for the centred mean)
   const graf_partials* stats;  // combined partials [B] for K_PASS2
@@ -1005,7 +1013,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       if (lrow) {
         const Mask inm = band & ~((k < 0 ? -k : k) <= p.ml_k ? mlb : (Mask)0);   // (CROSS rows may be k < 0)
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
-        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f, rowC1 = 0.f, rowM1 = -INFINITY;
+        float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f, rowC1 = 0.f, rowM1 = -INFINITY, rowX = 0.f;
         const float gsc = scaleG * mult;
         // match targets of rows +k and -k (K_MATCH; the host checked the window holds them)
         const float* tgp = nullptr;
@@ -1093,7 +1101,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               argK = better ? key : argK;
             }
           } else if constexpr (KIND == K_ISL) {
-            v[e] = cscale(v[e], in ? p.lam_isl * w * gsc : 0.f);   // G (x2 for a folded row pair)
+            if (p.complement) {   // f' = -lambda_isl on the excluded (mainlobe) cells only
+              v[e] = cscale(v[e], in ? 0.f : -p.lam_isl * gsc);
+              rowX += in ? 0.f : chi;
+            } else {
+              v[e] = cscale(v[e], in ? p.lam_isl * w * gsc : 0.f);   // G (x2 for a folded row pair)
+            }
           } else if constexpr (KIND == K_MATCH) {
             // f' of the folded pair (k, m), (-k, -m) / mult: lambda (2x - t1 - t2); a row that is
             // its own mirror uses t2 = t1
@@ -1119,18 +1132,18 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               rowC1 += in ? ec : 0.f;                      // (single pass: Z_c and the validity max)
               rowM1 = fmaxf(rowM1, in ? x : -INFINITY);
             } else {
-              fp = p.lam_isl * w + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
+              fp = (p.const_sum || p.complement ? 0.f : p.lam_isl * w) + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
 #ifdef GRAF_MUTATE_NO_PSL
               fp = p.lam_isl * w;
 #endif
             }
-            fp = in ? fp : 0.f;
+            fp = in ? fp : (p.complement ? -p.lam_isl : 0.f);
             rowF = fmaf(fp, chi, rowF);
             v[e] = cscale(v[e], fp * gsc);
           }
         }
         }
-        if constexpr (KIND == K_ISL) rowF = p.lam_isl * rowS;
+        if constexpr (KIND == K_ISL) rowF = p.complement ? -p.lam_isl * rowX : p.lam_isl * rowS;
         accS += (double)(mult * rowS);
         accF += (double)(mult * rowF);
         if constexpr (KIND == K_MATCH) accMt += (double)rowMt;
