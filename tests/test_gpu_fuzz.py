@@ -130,3 +130,46 @@ def test_fuzz_large_m_narrow_band(case):
         assert abs(loss[b] - L_ref) <= 1e-4 * abs(L_ref) + 1e-30, (ctx, loss[b], L_ref)
         tol = grad_tol(g_ref, t["sigma_g"])
         assert np.abs(g[b] - g_ref).max() <= tol + 1e-30, (ctx, np.abs(g[b] - g_ref).max(), tol)
+
+
+@pytest.mark.parametrize("case", range(32))
+def test_fuzz_tmem_sizes(case):
+    """M = 8192 and 16384 (the tensor-memory accumulator kernels; M = 8192 with the unpadded
+    staged s): random N <= 1100, full or partial delay extents, mainlobe blocks, ISL / soft-PSL
+    / both, raw or normalised, surfaces on random windows, and the backward on a random
+    window, against the oracle (plain-relative gradient gate)."""
+    r = SplitMix64(0x7E3E0000 + case)
+    M = [8192, 16384][randint(r, 0, 1)]
+    N = randint(r, 2, 1100)
+    full = r.uniform(1)[0] < 0.4
+    ml_k, ml_d = randint(r, 0, 2), randint(r, 0, 2)
+    ml_k = min(ml_k, N - 1)
+    k_max = N - 1 if full else randint(r, max(ml_k, 1), N - 1)
+    d_max = M // 2 if full else randint(r, ml_d + 1, 600)
+    lam_psl = [0.0, 1.0, 0.5][randint(r, 0, 2)]
+    lam_isl = 1.0 if lam_psl == 0.0 else [0.0, 1.0][randint(r, 0, 1)]
+    normalize = 1 if (lam_psl > 0 or r.uniform(1)[0] < 0.7) else 0
+    spec = dict(k_max=k_max, d_max=d_max, ml_k=ml_k, ml_d=ml_d, lambda_isl=lam_isl, lambda_psl=lam_psl,
+                temperature=[0.02, 0.05][randint(r, 0, 1)], normalize=normalize)
+    B = randint(r, 1, 2)
+    s = np.stack([complex_gaussian(SplitMix64(case * 131 + b), N) for b in range(B)])
+    kb = randint(r, -(N - 1), N - 1)
+    ke = randint(r, kb + 1, min(N, kb + 24))
+    kw = dict(out="c64", layout=["raw", "centered"][randint(r, 0, 1)], k_begin=kb, k_end=ke) \
+        if r.uniform(1)[0] < 0.4 else {}
+    loss, g, surf = graf.af_loss_grad(dev(s), M, graf.LossSpec.from_dict(spec), **kw)
+    loss, g = loss.cpu().numpy(), g.cpu().numpy()
+    ospec = O.LossSpec.from_dict(spec)
+    for b in range(B):
+        L_ref, g_ref, t = O.loss_and_grad(s[b], M, ospec)
+        ctx = (case, N, M, spec, b)
+        assert abs(loss[b] - L_ref) <= 1e-4 * abs(L_ref) + 1e-30, (ctx, loss[b], L_ref)
+        assert np.abs(g[b] - g_ref).max() <= grad_tol(g_ref, t["sigma_g"]) + 1e-30, (ctx, np.abs(g[b] - g_ref).max())
+        if kw:
+            ref = O.surface(s[b], M, "c64", kw["layout"], k_begin=kb, k_end=ke)
+            assert np.abs(surf[b].cpu().numpy() - ref).max() <= 1e-5 * O.energy(s[b]), ctx
+    rows = np.arange(kb, ke)
+    dA = complex_gaussian(SplitMix64(case + 11), len(rows) * M).reshape(1, len(rows), M)
+    gb = graf.af_backward(dev(s[:1]), M, dev(dA), k_begin=kb, k_end=ke, layout="raw").cpu().numpy()[0]
+    ref = O.adjoint(s[0], M, dA[0].astype(np.complex128), rows)
+    assert np.abs(gb - ref).max() <= 1e-4 * np.abs(ref).max(), (case, N, M, kb, ke)
