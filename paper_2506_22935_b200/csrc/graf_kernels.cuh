@@ -1015,6 +1015,23 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
         float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f, rowC1 = 0.f, rowM1 = -INFINITY, rowX = 0.f;
         const float gsc = scaleG * mult;
+        // ISL cotangent factors inside / outside the region (complement form: f' = -lambda_isl
+        // on the excluded mainlobe block only, nothing inside)
+        const float isl_in = p.complement ? 0.f : p.lam_isl * gsc;
+        const float lam_isl_in = (p.const_sum || p.complement) ? 0.f : p.lam_isl;   // pass 2
+        const float lam_isl_out = p.complement ? -p.lam_isl : 0.f;
+        const float isl_out = p.complement ? -p.lam_isl * gsc : 0.f;
+        if constexpr (KIND == K_ISL) {
+          // complement form: sum f' chi over the excluded cells = -lambda_isl sum chi over the
+          // mainlobe block, present in rows |k| <= ml_k only (before G overwrites v)
+          if (p.complement && (k < 0 ? -k : k) <= p.ml_k) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
+              rowX += ((mlb >> e) & 1) ? chi : 0.f;
+            }
+          }
+        }
         // match targets of rows +k and -k (K_MATCH; the host checked the window holds them)
         const float* tgp = nullptr;
         const float* tgn = nullptr;
@@ -1101,12 +1118,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               argK = better ? key : argK;
             }
           } else if constexpr (KIND == K_ISL) {
-            if (p.complement) {   // f' = -lambda_isl on the excluded (mainlobe) cells only
-              v[e] = cscale(v[e], in ? 0.f : -p.lam_isl * gsc);
-              rowX += in ? 0.f : chi;
-            } else {
-              v[e] = cscale(v[e], in ? p.lam_isl * w * gsc : 0.f);   // G (x2 for a folded row pair)
-            }
+            v[e] = cscale(v[e], in ? isl_in * w : isl_out);   // G (x2 for a folded row pair)
           } else if constexpr (KIND == K_MATCH) {
             // f' of the folded pair (k, m), (-k, -m) / mult: lambda (2x - t1 - t2); a row that is
             // its own mirror uses t2 = t1
@@ -1132,12 +1144,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               rowC1 += in ? ec : 0.f;                      // (single pass: Z_c and the validity max)
               rowM1 = fmaxf(rowM1, in ? x : -INFINITY);
             } else {
-              fp = (p.const_sum || p.complement ? 0.f : p.lam_isl * w) + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
+              fp = lam_isl_in * w + p.lam_psl * exp_fast((x - lse) * p.invT);   // lse = +inf without soft-PSL
 #ifdef GRAF_MUTATE_NO_PSL
               fp = p.lam_isl * w;
 #endif
             }
-            fp = in ? fp : (p.complement ? -p.lam_isl : 0.f);
+            fp = in ? fp : lam_isl_out;
             rowF = fmaf(fp, chi, rowF);
             v[e] = cscale(v[e], fp * gsc);
           }
