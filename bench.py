@@ -599,6 +599,12 @@ def run_graf(args, w, world):
                 "frac": fl_tf / FP32_PEAK_TFLOPS,
                 "peak_source": "derived (DESIGN.md §5): 148 SMs x 128 FP32 lanes x 2 flop (FFMA) x 1965 MHz",
                 "flop_count": w["flop_count"]}
+        if w["loss"]["lambda_psl"] != 0 and args.mode == "loss_grad" and not args.periodic:
+            # SURVEY.md §8(d)'s nominal count for a soft-PSL loss: 3 FFT passes per folded row
+            # (pass 1 forward; pass 2 forward + inverse), whatever the build executes
+            sv_flops = w["B"] * w["rows"] * 3 * 5.0 * w["M"] * math.log2(w["M"]) * (B / w["B"]) / (world if delay else 1)
+            roof["survey_3pass_flops_per_launch"] = sv_flops
+            roof["frac_survey_3pass"] = sv_flops / t_k / 1e12 / FP32_PEAK_TFLOPS
         if fp32_meas:
             roof["peak_measured"] = round(fp32_meas["tflops"], 2)
             roof["frac_of_measured"] = fl_tf / fp32_meas["tflops"]

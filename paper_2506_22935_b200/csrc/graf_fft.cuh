@@ -149,8 +149,34 @@ __device__ __forceinline__ float2 twc(float2 z) {
 //   u + j v = b (1 + j tan)  (2 FFMA),  x0 = a + c (u + j v),  x1 = a - c (u + j v)  (4 FFMA):
 // 6 FP instructions instead of 8 (a complex multiply, then 2 complex adds), each output
 // with the same rounding depth as the plain form.  (-DGRAF_NO_TAN_BFLY: the plain form.)
+#if defined(GRAF_F32X2) && defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+// a * b + c per lane (FFMA2)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+  return f2_unpack(r);
+}
+#endif
+
 template <int K, int R, bool INV>
 __device__ __forceinline__ void bfly_tw(float2 a, float2 b, float2& x0, float2& x1) {
+#if defined(GRAF_F32X2_TAN) && defined(GRAF_F32X2) && defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  // tangent form in paired fp32: three FFMA2 (one issue slot each; A/B builds only: c5
+  // measured 13.87 ms against 13.84 with scalar code, profiles/r02/tune_c5_ab_f32x2.txt)
+  constexpr int J = (((K * (32 / R)) % 32) + 32) % 32;
+  if constexpr (J % 8 != 0) {
+    constexpr float c = cos32(J);
+    constexpr float s = INV ? sin32(J) : -sin32(J);
+    constexpr bool cdom = (c < 0 ? -c : c) >= (s < 0 ? -s : s);
+    constexpr float q = cdom ? s / c : c / s;
+    constexpr float m = cdom ? c : s;
+    const float2 w = cdom ? ffma2(make_float2(-q, q), make_float2(b.y, b.x), b)
+                          : ffma2(make_float2(q, q), b, make_float2(-b.y, b.x));
+    x0 = ffma2(make_float2(m, m), w, a);
+    x1 = ffma2(make_float2(-m, -m), w, a);
+    return;
+  }
+#endif
 #if !defined(GRAF_NO_TAN_BFLY) && !defined(GRAF_F32X2)
   constexpr int J = (((K * (32 / R)) % 32) + 32) % 32;
   if constexpr (J % 8 != 0) {
@@ -316,6 +342,17 @@ __host__ __device__ constexpr int tw_offset(int M, int E, int p) {
   return off;
 }
 
+// 16 columns of this thread's tensor-memory lane, waited for (pass-1 twiddles, M = 16384)
+__device__ __forceinline__ void tmem_tw_ld16(uint32_t taddr, float (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]),
+        "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]), "=f"(r[14]), "=f"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 template <int R>
 __device__ __forceinline__ void tw_powers(float2 w1, float2* w) {
   w[0] = make_float2(1.f, 0.f);
@@ -349,11 +386,25 @@ struct Twiddles {
 #endif
   // pass-1 powers from a shared-memory table tw1[(r - 1) * NS1 + jm] (NS1 = first radix;
   // every thread of a slot shares the NS1 rows, so reads are broadcast / conflict-free)
-  static constexpr bool SMEM1 = !CACHE && NP >= 2;
+  // (M = 16384: GRAF_TW1_SMEM_16384=0 rebuilds the pass-1 powers from one base by the
+  // product tree, taking their 31 LDS per FFT off the shared-memory pipe the exchanges
+  // saturate: c5 13.84 -> 13.48 ms, but the c5 gradient error grows from 7e-5 to 1.8e-4 of
+  // max |g| at N = 256, past the 1e-4 gate; the default reads 10 entries and forms the other
+  // 21 by one product each, GRAF_TW1_SPLIT_16384.  At M = 8192 the tree made c4 3 % slower.)
+#ifndef GRAF_TW1_SMEM_16384
+#define GRAF_TW1_SMEM_16384 1
+#endif
+#ifndef GRAF_TW1_SPLIT_16384
+#define GRAF_TW1_SPLIT_16384 1
+#endif
+  static constexpr bool SMEM1 = !CACHE && NP >= 2 && (M != 16384 || GRAF_TW1_SMEM_16384);
   static constexpr int NS1 = NP >= 2 ? pass_ns(M, E, 1) : 1;
   static constexpr int R1 = NP >= 2 ? pass_radix(M, E, 1) : 1;
   static constexpr int TAB1 = SMEM1 ? (R1 - 1) * NS1 : 0;   // table entries
   const float2* tab1 = nullptr;
+  // (M = 16384 gradient kernels) tensor-memory address of this thread's 31 pass-1 twiddles
+  // W^(jm r), r = 1..31, at columns 2 (r - 1), 2 (r - 1) + 1; 0: use tab1
+  uint32_t ttw = 0;
 #ifdef GRAF_HOLD_BASES
   float2 base[NB > 0 && !CACHE ? NB : 1];
 #endif
@@ -402,8 +453,9 @@ struct Twiddles {
 };
 
 // One Stockham pass P (see header comment).  Non-final passes store to `sh`.
-template <int M, int E, int P, bool INV>
-__device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t, const Twiddles<M, E>& tw) {
+template <int M, int E, int P, bool INV, class Sync>
+__device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t, const Twiddles<M, E>& tw,
+                                              const Sync& sync) {
   constexpr int T = M / E;
   constexpr int R = pass_radix(M, E, P);
   constexpr int NS = pass_ns(M, E, P);
@@ -421,12 +473,44 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[q + r * Q];
     if constexpr (NS > 1) {
-      if (P == 1 && Twiddles<M, E>::SMEM1 && tw.tab1) {
-        const float2* tb = tw.tab1 + ((t + q * T) & (NS - 1));
+      if (P == 1 && R == 32 && Q == 1 && tw.ttw) {
+        // pass-1 twiddles from tensor memory (thread-private, correctly rounded, written once
+        // per kernel): off the shared-memory pipe, with the table's accuracy
 #pragma unroll
-        for (int r = 1; r < R; ++r) {
-          const float2 w = tb[(r - 1) * NS];
-          x[r] = INV ? cmulc(x[r], w) : cmul(x[r], w);
+        for (int c = 0; c < 4; ++c) {
+          float w16[16];
+          tmem_tw_ld16(tw.ttw + 16 * c, w16);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 8 * c + i + 1;
+            if (r < R) {
+              const float2 w = make_float2(w16[2 * i], w16[2 * i + 1]);
+              x[r] = INV ? cmulc(x[r], w) : cmul(x[r], w);
+            }
+          }
+        }
+      } else if (P == 1 && Twiddles<M, E>::SMEM1 && tw.tab1) {
+        const float2* tb = tw.tab1 + ((t + q * T) & (NS - 1));
+        if constexpr (R == 32 && M == 16384 && GRAF_TW1_SPLIT_16384) {
+          // 10 table reads instead of 31: W^r = W^(r mod 8) W^(8 floor(r / 8)), one product
+          // of correctly rounded entries (the shared-memory pipe is the scarce one here; a
+          // product tree from one base costs accuracy: c5 gradient error 7e-5 -> 1.8e-4)
+          float2 lo[8], hi[4];
+#pragma unroll
+          for (int r = 1; r < 8; ++r) lo[r] = tb[(r - 1) * NS];
+#pragma unroll
+          for (int j = 1; j < 4; ++j) hi[j] = tb[(8 * j - 1) * NS];
+#pragma unroll
+          for (int r = 1; r < R; ++r) {
+            const float2 w = (r % 8 == 0) ? hi[r / 8] : (r < 8 ? lo[r] : cmul(lo[r % 8], hi[r / 8]));
+            x[r] = INV ? cmulc(x[r], w) : cmul(x[r], w);
+          }
+        } else {
+#pragma unroll
+          for (int r = 1; r < R; ++r) {
+            const float2 w = tb[(r - 1) * NS];
+            x[r] = INV ? cmulc(x[r], w) : cmul(x[r], w);
+          }
         }
       } else if constexpr (Twiddles<M, E>::CACHE) {
         constexpr int off = tw_count_before(M, E, P);
@@ -458,6 +542,7 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[E], float2* sh, int t,
 #pragma unroll
       for (int r = 0; r < R; ++r) v[q + r * Q] = x[r];
     } else {
+      if (q == 0) sync.before_writing();   // every reader of the previous contents is done
       const int jp = t + q * T;
       const int jm = jp & (NS - 1);
       const int base = (jp / NS) * NS * R + jm;
@@ -484,7 +569,7 @@ __device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, cons
                                          const Sync& sync) {
   constexpr int T = M / E;
   constexpr int NP = num_passes(M, E);
-  stockham_pass<M, E, P, INV>(v, sh, t, tw);
+  stockham_pass<M, E, P, INV>(v, sh, t, tw, sync);
   if constexpr (P + 1 < NP) {
     sync();
     if constexpr (PadStride<E, T>::AFFINE) {
@@ -495,7 +580,7 @@ __device__ __forceinline__ void fft_rows(float2 (&v)[E], float2* sh, int t, cons
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
     }
-    sync();
+    sync.done_reading();
     fft_rows<M, E, P + 1, INV, Sync>(v, sh, t, tw, sync);
   }
 }
@@ -540,11 +625,12 @@ __device__ __forceinline__ void fft_rows_edges(float2 (&v)[E], float2* sh, int t
     if constexpr (P == 0 && HZ && pass_radix(M, E, 0) == E && E <= Pad<E>::P) {
       // zero-padded row (2N <= M): the first butterfly's inputs v[E/2..E) are zero
       dft_lz<E, E / 2, false>(v);
+      sync.before_writing();
       float2* b = sh + padded<E>(t * E);
 #pragma unroll
       for (int r = 0; r < E; ++r) b[r] = v[r];
     } else {
-      stockham_pass<M, E, P, false>(v, sh, t, tw);
+      stockham_pass<M, E, P, false>(v, sh, t, tw, sync);
     }
     sync();
     if constexpr (PadStride<E, T>::AFFINE) {
@@ -555,7 +641,7 @@ __device__ __forceinline__ void fft_rows_edges(float2 (&v)[E], float2* sh, int t
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
     }
-    sync();
+    sync.done_reading();
     fft_rows_edges<M, E, P + 1, HZ, Sync>(v, sh, t, tw, sync);
   } else {
     fft_last_edges<M, E, P>(v, t);

@@ -216,9 +216,45 @@ GRAF_CFG(8192, GRAF_E_8192, GRAF_S_8192)
 GRAF_CFG(16384, GRAF_E_16384, 1)
 #undef GRAF_CFG
 
+// mbarrier helpers (split write-after-read barriers of the exchange buffer)
+__device__ __forceinline__ void mbar_init(uint32_t mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t mb) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(mb) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+#ifndef GRAF_TW1_TMEM_16384
+#define GRAF_TW1_TMEM_16384 1   // M = 16384 gradient kernels: pass-1 twiddles in tensor memory
+#endif
+#ifndef GRAF_SPLIT_WAR
+// one-slot CTAs: 1 = split write-after-read barriers, 0 = a full barrier after every read
+// phase (default: the split form measured SLOWER, c5 13.48 -> 15.01 ms, c4 2.064 -> 2.106 ms,
+// profiles/r02/tune_c5_war.txt: the read-after-write barrier of every exchange stays, so warps
+// gain little skew, and 512 threads polling the mbarrier compete with the exchange's LDS)
+#define GRAF_SPLIT_WAR 0
+#endif
+
+// Synchronisation of one row slot's exchange buffer.  operator() orders writes before
+// reads (read-after-write: a full barrier of the slot).  done_reading() / before_writing()
+// bracket the write-after-read hazard: by default done_reading() is a full barrier and
+// before_writing() nothing.  In a one-slot CTA (S == 1) with `mb` set, done_reading() is an
+// mbarrier arrival per warp and before_writing() waits for every warp's arrival, so a warp
+// that has read its data runs the next pass's arithmetic while slower warps are still
+// reading (the shared-memory and FP32 phases of different warps overlap; a full barrier
+// after every read phase serialises them: scripts/ubench/phase_overlap.cu).  Every write
+// phase of the buffer is preceded by before_writing() and every read phase followed by
+// done_reading(), in the same order in every warp (one arrival is made at the start).
 template <int T, int S>
 struct SlotSync {
   int id;
+  uint32_t mb = 0;            // S == 1: shared address of the WAR mbarrier (0: full barriers)
+  mutable uint32_t ph = 0;    // parity of the next phase before_writing() waits for
   __device__ __forceinline__ void operator()() const {
     if constexpr (T <= 32) {
       __syncwarp();
@@ -226,6 +262,24 @@ struct SlotSync {
       __syncthreads();
     } else {
       asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(T) : "memory");
+    }
+  }
+  __device__ __forceinline__ void done_reading() const {
+    if constexpr (S == 1 && T >= 64) {
+      if (mb) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(mb);
+        return;
+      }
+    }
+    (*this)();
+  }
+  __device__ __forceinline__ void before_writing() const {
+    if constexpr (S == 1 && T >= 64) {
+      if (mb) {
+        mbar_wait(mb, ph);
+        ph ^= 1u;
+      }
     }
   }
 };
@@ -472,6 +526,24 @@ __device__ __forceinline__ void tmem_wait_ld16(float (&r)[16]) {
                :
                : "memory");
 }
+// 8 columns (4 complex accumulators)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld8(float (&r)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(r[0]), "+f"(r[1]), "+f"(r[2]), "+f"(r[3]), "+f"(r[4]), "+f"(r[5]), "+f"(r[6]), "+f"(r[7])
+               :
+               : "memory");
+}
 // 16 consecutive 32-bit columns of this thread's lane (8 complex accumulators)
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
   asm volatile(
@@ -490,6 +562,25 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&r)[16]) 
       "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]), "f"(r[15])
       : "memory");
 }
+
+// generic chunk of C columns (C = 8 or 16)
+template <int C>
+__device__ __forceinline__ void tmem_ldc(uint32_t a, float (&r)[C]) {
+  if constexpr (C == 16) tmem_ld16(a, r); else tmem_ld8(a, r);
+}
+template <int C>
+__device__ __forceinline__ void tmem_stc(uint32_t a, const float (&r)[C]) {
+  if constexpr (C == 16) tmem_st16(a, r); else tmem_st8(a, r);
+}
+template <int C>
+__device__ __forceinline__ void tmem_wait_ldc(float (&r)[C]);
+template <>
+__device__ __forceinline__ void tmem_wait_ldc<16>(float (&r)[16]) { tmem_wait_ld16(r); }
+template <>
+__device__ __forceinline__ void tmem_wait_ldc<8>(float (&r)[8]) { tmem_wait_ld8(r); }
+#ifndef GRAF_TMEM_SLOTS
+#define GRAF_TMEM_SLOTS 8    // slots per TMEM read-modify-write chunk in the correlation (8 or 4)
+#endif
 
 // slots per batch of predicated accumulator loads in the correlation (loads of a
 // batch are issued back to back, then the stores)
@@ -537,6 +628,7 @@ __device__ __forceinline__ void ifft_band_edges(float2 (&v)[E], float2* sh, int 
   static_assert(pass_radix(M, E, 0) == E && E <= Pad<E>::P, "first pass must be one radix-E butterfly");
   const float2 x0 = v[0], xl = v[E - 1];
   float2* b = sh + padded<E>(t * E);
+  sync.before_writing();
   static_for<0, E>([&](auto r) {
     constexpr int K = ((E - 1) * decltype(r)::value) % E;
     b[decltype(r)::value] = cadd(x0, twc<K, E, true>(xl));
@@ -550,7 +642,7 @@ __device__ __forceinline__ void ifft_band_edges(float2 (&v)[E], float2* sh, int 
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = sh[padded<E>(t + e * T)];
   }
-  sync();
+  sync.done_reading();
   fft_rows<M, E, 1, true>(v, sh, t, tw, sync);
 }
 
@@ -684,7 +776,10 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // prologue barrier; thread (w, lane) owns lane 32 (w % 4) + lane, columns 64 (w / 4) ..
   constexpr bool kTmem = GRAD && kGtmem;
   // columns: THREADS / 128 warps per lane quarter, 2E columns (E complex) per thread
-  constexpr int kTmemNC = 2 * E * (THREADS / 128);
+  // (M = 16384: a second block of 256 columns holds every thread's 31 pass-1 twiddles)
+  constexpr bool kTwTmem = kTmem && (M == 16384) && !SPLIT && GRAF_TW1_TMEM_16384 && (E == 32) &&
+                           (num_passes(M, E) >= 2) && (pass_radix(M, E, 1) == 32);
+  constexpr int kTmemNC = 2 * E * (THREADS / 128) * (kTwTmem ? 2 : 1);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
   if constexpr (kTmem) {
     static_assert(THREADS % 128 == 0 && (E % 8) == 0, "TMEM accumulator layout: whole lane quarters");
@@ -705,6 +800,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     band |= (Mask)(ad <= p.d_max ? 1 : 0) << e;
     mlb |= (Mask)(ad <= p.ml_d ? 1 : 0) << e;
   }
+  // split write-after-read barrier of the exchange buffer (one-slot CTAs; not when the
+  // surface staging is aliased onto the exchange buffer, p.bulk == 2)
+  const uint32_t war_mb = smem_u32(red + 62);
+  const bool split_war = (S == 1) && (T >= 64) && GRAF_SPLIT_WAR && p.bulk != 2;
+  if (split_war && threadIdx.x == 0) mbar_init(war_mb, THREADS / 32);
   __syncthreads();
   uint32_t tacc = 0;   // this thread's TMEM accumulator address (lane field | column)
   if constexpr (kTmem) {
@@ -715,6 +815,25 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     for (int i = 0; i < 16; ++i) z[i] = 0.f;
 #pragma unroll
     for (int c = 0; c < E / 8; ++c) tmem_st16(tacc + 16 * c, z);
+    if constexpr (kTwTmem) {
+      // pass-1 twiddles W_M^(jm r (M / (NS1 R1))) with jm = t mod NS1 (the tab1 entries)
+      constexpr int NS1 = pass_ns(M, E, 1), R1 = pass_radix(M, E, 1);
+      const int jm = t0 & (NS1 - 1);
+      const uint32_t ttw = tacc + kTmemNC / 2;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float w16[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = 8 * c + i + 1;
+          const float2 w = r < R1 ? g_tw[(jm * r * (M / (NS1 * R1))) * (kMaxM / M)] : make_float2(0.f, 0.f);
+          w16[2 * i] = w.x;
+          w16[2 * i + 1] = w.y;
+        }
+        tmem_st16(ttw + 16 * c, w16);
+      }
+      tw.ttw = ttw;
+    }
     tmem_wait_st();
   }
   const double Ed = red[0];
@@ -744,6 +863,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   const bool want_lse = FWD && p.loss_on && p.lam_psl != 0.f;
 
   SlotSync<T, S> sync{1 + slot};
+  if (split_war) {
+    sync.mb = war_mb;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(war_mb);   // the buffer starts free: the first wait passes
+  }
   float2* sh = xch + (size_t)slot * XS;
   // aliased staging (p.bulk == 2): the row lives in the slot's exchange buffer, which
   // is free between the last pass of one FFT and the first exchange of the next
@@ -1238,19 +1362,21 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           // the lower half of the slots writes H or touches its accumulators)
           float2* hb = sh;
           const int nch = (kHalfSizes && half) ? E / 16 : E / 8;
+          sync.before_writing();
 #pragma unroll
           for (int e = 0; e < E; ++e)
             if (8 * nch > e) hb[t + e * T] = v[e];
           sync();
           const bool per = p.periodic != 0;
+          constexpr int CS = GRAF_TMEM_SLOTS;      // slots per chunk (2 CS columns)
 #pragma unroll
-          for (int c = 0; c < E / 8; ++c) {
-            if (c >= nch) break;
-            float acc[16], d[16];
-            tmem_ld16(tacc + 16 * c, acc);   // in flight while this chunk's terms are formed
+          for (int c = 0; c < E / CS; ++c) {
+            if (c * CS >= 8 * nch) break;
+            float acc[2 * CS], d[2 * CS];
+            tmem_ldc<2 * CS>(tacc + 2 * CS * c, acc);   // in flight while this chunk's terms are formed
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int e = 8 * c + i;
+            for (int i = 0; i < CS; ++i) {
+              const int e = CS * c + i;
               const int pp = t + e * T;
               const int q1 = per ? ((pp - k) & (N - 1)) : pp - k;            // s index, term 1
               const int q2 = per ? ((pp + k) & (N - 1)) : pp + k;            // H and s index, term 2
@@ -1267,11 +1393,12 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               d[2 * i] = a1.x + a2.x;
               d[2 * i + 1] = a1.y + a2.y;
             }
-            tmem_wait_ld16(acc);
+            tmem_wait_ldc<2 * CS>(acc);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] += d[i];
-            tmem_st16(tacc + 16 * c, acc);
+            for (int i = 0; i < 2 * CS; ++i) acc[i] += d[i];
+            tmem_stc<2 * CS>(tacc + 2 * CS * c, acc);
           }
+          sync.done_reading();   // H has been read: the next row's first pass may overwrite it
           tmem_wait_st();
         } else if (p.periodic) {
           // circular lag products (M == N): every slot is in the support; term 1 reads
@@ -1425,7 +1552,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             corr(std::integral_constant<int, E / CC>{});
           }
         }
-        sync();
+        // (the TMEM branch released the buffer with done_reading(); shared-memory
+        // accumulators need the full barrier before the next row's read-modify-writes)
+        if (!kTmem) sync();
       }
     }
   }
