@@ -578,6 +578,9 @@ template <>
 __device__ __forceinline__ void tmem_wait_ldc<16>(float (&r)[16]) { tmem_wait_ld16(r); }
 template <>
 __device__ __forceinline__ void tmem_wait_ldc<8>(float (&r)[8]) { tmem_wait_ld8(r); }
+#ifndef GRAF_SOWN_TMEM_16384
+#define GRAF_SOWN_TMEM_16384 1   // M = 16384 gradient kernels: own samples in TMEM (see kSown)
+#endif
 #ifndef GRAF_TMEM_SLOTS
 #define GRAF_TMEM_SLOTS 8    // slots per TMEM read-modify-write chunk in the correlation (8 or 4)
 #endif
@@ -777,9 +780,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   constexpr bool kTmem = GRAD && kGtmem;
   // columns: THREADS / 128 warps per lane quarter, 2E columns (E complex) per thread
   // (M = 16384: a second block of 256 columns holds every thread's 31 pass-1 twiddles)
-  constexpr bool kTwTmem = kTmem && (M == 16384) && !SPLIT && GRAF_TW1_TMEM_16384 && (E == 32) &&
+  // (GRAF_SOWN_TMEM_16384: the second block holds every thread's own samples s[t + eT] instead,
+  // written once per kernel; the lag product and the correlation's second term then read
+  // one sample per slot from L2 instead of two, and the pass-1 twiddles come from tab1)
+  constexpr bool kSown = kTmem && (M == 16384) && !SPLIT && !CROSS && GRAF_SOWN_TMEM_16384 && (E == 32);
+  constexpr bool kTwTmem = kTmem && !kSown && (M == 16384) && !SPLIT && GRAF_TW1_TMEM_16384 && (E == 32) &&
                            (num_passes(M, E) >= 2) && (pass_radix(M, E, 1) == 32);
-  constexpr int kTmemNC = 2 * E * (THREADS / 128) * (kTwTmem ? 2 : 1);
+  constexpr int kTmemNC = 2 * E * (THREADS / 128) * ((kTwTmem || kSown) ? 2 : 1);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
   if constexpr (kTmem) {
     static_assert(THREADS % 128 == 0 && (E % 8) == 0, "TMEM accumulator layout: whole lane quarters");
@@ -833,6 +840,20 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         tmem_st16(ttw + 16 * c, w16);
       }
       tw.ttw = ttw;
+    }
+    if constexpr (kSown) {
+      const float2* so = p.s_pad + (size_t)b * RP + NL + t0;   // zero beyond N
+#pragma unroll
+      for (int c = 0; c < E / 8; ++c) {
+        float f16[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 x = so[(8 * c + i) * T];
+          f16[2 * i] = x.x;
+          f16[2 * i + 1] = x.y;
+        }
+        tmem_st16(tacc + kTmemNC / 2 + 16 * c, f16);
+      }
     }
     tmem_wait_st();
   }
@@ -970,8 +991,28 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         } else if constexpr (!C::S_SMEM || kStrim) {
           // global s copy (M = 16384) or the unpadded smem copy (M = 8192): slots outside the
           // row's support load nothing; their lag products are exactly zero
+          if constexpr (kSown) {
+            // s[n] from this thread's tensor-memory copy, s[n - k] from L2: every load of the
+            // row is issued before the first tcgen05.ld (whose memory clobber orders them)
+            // (predicated to the row's support: unconditional loads from the zero padding
+            // measured slower, 13.52 vs 12.96 ms, profiles/r02/tune_c5_sown_affine.txt)
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = ((vmask >> e) & 1) ? c[e * T] : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int cc = 0; cc < E / 8; ++cc) {
+              float xs[16];
+              tmem_ld16(tacc + kTmemNC / 2 + 16 * cc, xs);
+              tmem_wait_ld16(xs);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[8 * cc + i] = cmulc(make_float2(xs[2 * i], xs[2 * i + 1]), v[8 * cc + i]);
+            }
+          } else
 #pragma unroll
           for (int e = 0; e < E; ++e) {
+#ifdef GRAF_ABL_NO_LAG   // timing ablation only (scripts/tune.py): no loads, synthetic row
+            v[e] = make_float2(1e-3f * (float)(t + e), 1e-3f * (float)k);
+            continue;
+#endif
             float2 x = make_float2(0.f, 0.f), y = x;
             if ((vmask >> e) & 1) {
               x = a[e * T];
@@ -1336,7 +1377,9 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         stg_release();
         if constexpr (kEdgeBand) {
           if (edge_band) ifft_band_edges<M, E>(v, sh, t, tw, sync);
+#ifndef GRAF_ABL_NO_INV   // timing ablation only
           else row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
+#endif
         } else {
 #ifndef GRAF_ABL_NO_INV   // timing ablation only
           row_fft<M, E, SPLIT, true>(v, sh, t, tw, sync, wt);
@@ -1352,6 +1395,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
         const int tb = SPLIT ? 2 * t : t;
         // predicated shared-memory read-modify-writes (no branches; an out-of-support
         // slot neither loads nor stores its accumulator)
+#ifdef GRAF_ABL_NO_CORR   // timing ablation only: keep v live, skip the correlation
+        if constexpr (kTmem) {
+          if (v[0].x == 1234.5f) p.gpart[t] = v[1];
+        } else
+#endif
         if constexpr (kTmem) {
           // Both terms accumulate at the thread's OWN positions p = t + eT, so the
           // accumulator is thread-private (TMEM):
@@ -1363,12 +1411,64 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           float2* hb = sh;
           const int nch = (kHalfSizes && half) ? E / 16 : E / 8;
           sync.before_writing();
+          if constexpr (kSown) {
+            // term 2 needs conj(H[q]) s[q] at q = p + k: form it at the owner of q (s[q] from
+            // tensor memory) and pass the product through the exchange buffer
 #pragma unroll
-          for (int e = 0; e < E; ++e)
-            if (8 * nch > e) hb[t + e * T] = v[e];
+            for (int cc = 0; cc < E / 8; ++cc) {
+              if (8 * cc >= 8 * nch) break;
+              float xs[16];
+              tmem_ld16(tacc + kTmemNC / 2 + 16 * cc, xs);
+              tmem_wait_ld16(xs);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                hb[t + (8 * cc + i) * T] = cmulc(make_float2(xs[2 * i], xs[2 * i + 1]), v[8 * cc + i]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              if (8 * nch > e) hb[t + e * T] = v[e];
+          }
           sync();
           const bool per = p.periodic != 0;
           constexpr int CS = GRAF_TMEM_SLOTS;      // slots per chunk (2 CS columns)
+          if (!per) {
+            // aperiodic rows: term 1 of slot e reads s at (t - k) + eT, term 2 the exchange
+            // buffer at (t + k) + eT: one base address each and immediate offsets; the
+            // supports are two slot masks (p in [lo, hi) and p + k in [lo, hi)), no per-slot
+            // index arithmetic
+            const int lo2 = lo - k, hi2 = hi - k;
+            const VMask m2 = lrow ? (VMask)slot_range_mask(lo2 > t ? (lo2 - t + T - 1) >> LT : 0,
+                                                           hi2 > t ? (hi2 - t + T - 1) >> LT : 0)
+                                  : (VMask)0;
+            const float2* s1p = sv + t - k;
+            const float2* s2p = sv + t + k;
+            const float2* h2p = hb + t + k;
+#pragma unroll
+            for (int c = 0; c < E / CS; ++c) {
+              if (c * CS >= 8 * nch) break;
+              float acc[2 * CS], d[2 * CS];
+              tmem_ldc<2 * CS>(tacc + 2 * CS * c, acc);
+#pragma unroll
+              for (int i = 0; i < CS; ++i) {
+                const int e = CS * c + i;
+                float2 s1 = make_float2(0.f, 0.f), s2 = s1, h2 = s1;
+                if ((m1 >> e) & 1) s1 = s1p[e * T];
+                if ((m2 >> e) & 1) {
+                  if constexpr (!kSown) s2 = s2p[e * T];
+                  h2 = h2p[e * T];
+                }
+                const float2 a1 = cmul(v[e], s1);
+                const float2 a2 = kSown ? h2 : cmulc(s2, h2);
+                d[2 * i] = a1.x + a2.x;
+                d[2 * i + 1] = a1.y + a2.y;
+              }
+              tmem_wait_ldc<2 * CS>(acc);
+#pragma unroll
+              for (int i = 0; i < 2 * CS; ++i) acc[i] += d[i];
+              tmem_stc<2 * CS>(tacc + 2 * CS * c, acc);
+            }
+          } else
 #pragma unroll
           for (int c = 0; c < E / CS; ++c) {
             if (c * CS >= 8 * nch) break;
@@ -1385,11 +1485,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
               float2 s1 = make_float2(0.f, 0.f), s2 = s1, h2 = s1;
               if (in1) s1 = sv[q1];
               if (in2) {
-                s2 = sv[q2];
+                if constexpr (!kSown) s2 = sv[q2];
                 h2 = hb[q2];
               }
               const float2 a1 = cmul(v[e], s1);
-              const float2 a2 = cmulc(s2, h2);      // conj(H) s
+              const float2 a2 = kSown ? h2 : cmulc(s2, h2);      // conj(H) s
               d[2 * i] = a1.x + a2.x;
               d[2 * i + 1] = a1.y + a2.y;
             }
