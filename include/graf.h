@@ -116,7 +116,12 @@ typedef struct {
   const float* w_k;         /* optional device [2N-1] delay weights */
   const float* w_d;         /* optional device [M] Doppler weights */
   float lambda_isl, lambda_psl;
-  float temperature;        /* T > 0 (read iff lambda_psl != 0) */
+  float temperature;        /* T > 0 (read iff lambda_psl != 0), in the units of x.  The kernels
+                               form (x - LSE)/T in fp32, so T must be well above the rounding of
+                               max x, ~6e-8 max x: with normalize = 1 (x <= 1) any T >= 1e-5 is
+                               safe (the configs use 0.01); with raw chi (x ~ E^2) T = 0.01 is
+                               below fp32 resolution and the soft-PSL gradient is not reliable
+                               (reading R30).  Not checked at run time. */
   int32_t normalize;        /* 1 (default reading R6) or 0 (raw chi) */
   float lambda_hpsl;        /* weight of the HARD PSL = max_{Omega} x (Eq. 19) with its
                                argmax subgradient (the paper's section-7 loss, L416); ties go to
