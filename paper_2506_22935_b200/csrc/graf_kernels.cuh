@@ -660,7 +660,9 @@ __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi
 // mirror symmetry), lag product s[n] conj(s2[n-k]), normalisation by E1 E2 (reading
 // R25), and the correlation split into dL/ds* (term 1, with s2) and dL/ds2* (term 2,
 // with s) accumulated separately.
-template <int M, int KIND, bool WGT, bool CROSS = false>
+// SURF = false: a loss-only instantiation with the surface epilogue compiled out (M >= 8192,
+// where the register budget is tight; the host picks it when the call writes no surface)
+template <int M, int KIND, bool WGT, bool CROSS = false, bool SURF = true>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
   // cross-ambiguity kernels keep the padded s and the shared-memory accumulators
@@ -1080,7 +1082,8 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       }
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
-      if (p.bulk) {
+      if (!SURF) {
+      } else if (p.bulk) {
         // dedicated staging: the slot's previous bulk copies must have finished reading it
         if (p.bulk == 1) {
           if (t0 == 0) bulk_wait_read_all();
