@@ -660,9 +660,11 @@ __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi
 // mirror symmetry), lag product s[n] conj(s2[n-k]), normalisation by E1 E2 (reading
 // R25), and the correlation split into dL/ds* (term 1, with s2) and dL/ds2* (term 2,
 // with s) accumulated separately.
-// SURF = false: a loss-only instantiation with the surface epilogue compiled out (M >= 8192,
-// where the register budget is tight; the host picks it when the call writes no surface)
-template <int M, int KIND, bool WGT, bool CROSS = false, bool SURF = true>
+// FLV (flavour, M >= 8192 where the register budget is tight; the host picks it per call):
+//   0 the general kernel;  1 loss-only, the surface epilogue compiled out (c4 -6 %, c5 -2.5 %,
+//   profiles/r02/tune_nosurf.txt).  (A third flavour with only the full-plane single pass
+//   compiled in spilled 352 B and measured 14.68 ms against 12.65: not kept.)
+template <int M, int KIND, bool WGT, bool CROSS = false, int FLV = 0>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af_rows_kernel(RowParams p) {
   using C = Cfg<M>;
   // cross-ambiguity kernels keep the padded s and the shared-memory accumulators
@@ -1082,7 +1084,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       }
 
       // ---- a3F: surface epilogue (rows +k and, folded, -k)
-      if (!SURF) {
+      if (FLV >= 1) {
       } else if (p.bulk) {
         // dedicated staging: the slot's previous bulk copies must have finished reading it
         if (p.bulk == 1) {

@@ -81,7 +81,7 @@ inline int choose_P(const Plan& pl, long long B, int occ, int nsm) {
   return best;
 }
 
-template <int M, int KIND, bool WGT, bool CROSS = false, bool SURF = true>
+template <int M, int KIND, bool WGT, bool CROSS = false, int FLV = 0>
 cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
   static std::once_flag once[kMaxDev];
   static cudaError_t attr_err[kMaxDev];
@@ -90,22 +90,22 @@ cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::call_once(once[dev], [dev] {
-    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M, KIND, WGT, CROSS, SURF>,
+    attr_err[dev] = cudaFuncSetAttribute(af_rows_kernel<M, KIND, WGT, CROSS, FLV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (attr_err[dev] == cudaSuccess)
       attr_err[dev] = cudaDeviceGetAttribute(&sm_count[dev], cudaDevAttrMultiProcessorCount, dev);
   });
   if (attr_err[dev] != cudaSuccess) return attr_err[dev];
   *nsm = sm_count[dev];
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT, CROSS, SURF>, Cfg<M>::THREADS,
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT, CROSS, FLV>, Cfg<M>::THREADS,
                                                        smem);
 }
 
-template <int M, int KIND, bool WGT, bool CROSS = false, bool SURF = true>
+template <int M, int KIND, bool WGT, bool CROSS = false, int FLV = 0>
 cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
   int occ = 1, nsm = device_sm_count();
   // (also sets the instantiation's large-shared-memory attribute, once per device)
-  cudaError_t e0 = kernel_occupancy<M, KIND, WGT, CROSS, SURF>(pl.smem, &occ, &nsm);
+  cudaError_t e0 = kernel_occupancy<M, KIND, WGT, CROSS, FLV>(pl.smem, &occ, &nsm);
   if (e0 != cudaSuccess) return e0;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   size_t smem = pl.smem;
@@ -115,7 +115,7 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
       int occ_g = 0;
       const bool fits = pl.smem + pl.smem_gpad <= 227 * 1024;
       if (fits) {
-        e0 = kernel_occupancy<M, KIND, WGT, CROSS, SURF>(pl.smem + pl.smem_gpad, &occ_g, &nsm);
+        e0 = kernel_occupancy<M, KIND, WGT, CROSS, FLV>(pl.smem + pl.smem_gpad, &occ_g, &nsm);
         if (e0 != cudaSuccess) return e0;
       }
       pl.gpad_mode = (fits && occ_g >= occ) ? 1 : 0;
@@ -131,7 +131,7 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
       int occ_d = 0;
       const bool fits = smem + pl.smem_stg <= 227 * 1024;
       if (fits) {
-        e0 = kernel_occupancy<M, KIND, WGT, CROSS, SURF>(smem + pl.smem_stg, &occ_d, &nsm);
+        e0 = kernel_occupancy<M, KIND, WGT, CROSS, FLV>(smem + pl.smem_stg, &occ_d, &nsm);
         if (e0 != cudaSuccess) return e0;
       }
       pl.bulk_mode = (fits && (occ_d >= occ || !pl.alias_ok) && occ_d >= 1) ? 1 : pl.alias_ok ? 2 : 0;
@@ -140,7 +140,7 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
     rp.stg_floats = pl.stg_floats;
     if (rp.bulk == 1) {
       smem += pl.smem_stg;
-      e0 = kernel_occupancy<M, KIND, WGT, CROSS, SURF>(smem, &occ, &nsm);
+      e0 = kernel_occupancy<M, KIND, WGT, CROSS, FLV>(smem, &occ, &nsm);
       if (e0 != cudaSuccess) return e0;
     }
   } else {
@@ -176,10 +176,10 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, af_rows_kernel<M, KIND, WGT, CROSS, SURF>, rp);
+      cudaError_t e = cudaLaunchKernelEx(&cfg, af_rows_kernel<M, KIND, WGT, CROSS, FLV>, rp);
       if (e != cudaSuccess) return e;
     } else {
-      af_rows_kernel<M, KIND, WGT, CROSS, SURF><<<grid, pl.threads, smem, st>>>(rp);
+      af_rows_kernel<M, KIND, WGT, CROSS, FLV><<<grid, pl.threads, smem, st>>>(rp);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -215,19 +215,19 @@ cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st,
       switch (kind) {
         case K_FWD:
           if (rp.want_argmax)
-            return wgt ? launch_kernel<M, K_FWDA, true, false, false>(pl, rp, B, st)
-                       : launch_kernel<M, K_FWDA, false, false, false>(pl, rp, B, st);
-          return wgt ? launch_kernel<M, K_FWD, true, false, false>(pl, rp, B, st)
-                     : launch_kernel<M, K_FWD, false, false, false>(pl, rp, B, st);
+            return wgt ? launch_kernel<M, K_FWDA, true, false, 1>(pl, rp, B, st)
+                       : launch_kernel<M, K_FWDA, false, false, 1>(pl, rp, B, st);
+          return wgt ? launch_kernel<M, K_FWD, true, false, 1>(pl, rp, B, st)
+                     : launch_kernel<M, K_FWD, false, false, 1>(pl, rp, B, st);
         case K_ISL:
-          return wgt ? launch_kernel<M, K_ISL, true, false, false>(pl, rp, B, st)
-                     : launch_kernel<M, K_ISL, false, false, false>(pl, rp, B, st);
+          return wgt ? launch_kernel<M, K_ISL, true, false, 1>(pl, rp, B, st)
+                     : launch_kernel<M, K_ISL, false, false, 1>(pl, rp, B, st);
         case K_PASS2:
-          return wgt ? launch_kernel<M, K_PASS2, true, false, false>(pl, rp, B, st)
-                     : launch_kernel<M, K_PASS2, false, false, false>(pl, rp, B, st);
+          return wgt ? launch_kernel<M, K_PASS2, true, false, 1>(pl, rp, B, st)
+                     : launch_kernel<M, K_PASS2, false, false, 1>(pl, rp, B, st);
         case K_MATCH:
-          return wgt ? launch_kernel<M, K_MATCH, true, false, false>(pl, rp, B, st)
-                     : launch_kernel<M, K_MATCH, false, false, false>(pl, rp, B, st);
+          return wgt ? launch_kernel<M, K_MATCH, true, false, 1>(pl, rp, B, st)
+                     : launch_kernel<M, K_MATCH, false, false, 1>(pl, rp, B, st);
         default: break;
       }
     }
