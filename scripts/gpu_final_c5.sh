@@ -17,5 +17,8 @@ timeout 1500 ncu --set full --clock-control none --import-source on --kernel-nam
 echo "ncu exit=$?"
 python scripts/ncu_summary.py gpurun_out/prof_${TAG}_c5.ncu-rep gpurun_out/sum_${TAG}_c5.txt > /dev/null 2>&1
 python scripts/ncu_mix.py gpurun_out/prof_${TAG}_c5.ncu-rep > gpurun_out/mix_${TAG}_c5.txt 2>&1
+ncu -i gpurun_out/prof_${TAG}_c5.ncu-rep --page source --csv --print-source sass > gpurun_out/sass_${TAG}_c5.csv 2>/dev/null
+python scripts/ncu_phases.py gpurun_out/sass_${TAG}_c5.csv > gpurun_out/phases_${TAG}_c5.txt 2>&1
+rm -f gpurun_out/sass_${TAG}_c5.csv
 SZ=$(stat -c %s gpurun_out/prof_${TAG}_c5.ncu-rep 2>/dev/null || echo 0)
 if [ "$SZ" -gt 25000000 ]; then rm -f gpurun_out/prof_${TAG}_c5.ncu-rep; fi
