@@ -53,7 +53,9 @@ def compile_link(out: str, sources, defines=(), objdir=None, verbose=False) -> N
     procs, objs = [], []
     for src in sources:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *CFLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+        # GRAF_EXTRA_NVCC: extra nvcc flags for tuning builds (scripts/tune.py); unset in product builds
+        extra = os.environ.get("GRAF_EXTRA_NVCC", "").split()
+        cmd = [nvcc(), *CFLAGS, *extra, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd))
