@@ -16,6 +16,11 @@ stored, so the c5 loss is isl + lse.
 
 Cost: three 32767 x 16384 x 16384 complex matrix products (~2.1e14 flops); ~25-40 min
 on 8 cores.  Run once:  python scripts/make_c5_golden.py
+
+`--lfm` writes tests/golden/c5_lfm_softpsl.npz instead: the same spec on an LFM chirp
+(graf_inputs.lfm(16384, beta = 1), phase pi n^2 / N).  Its delay-Doppler ridge puts
+max x - xbar far above 40 T, so the GPU's optimistic single pass (reading R13) is invalid
+for it and the guarded two-pass fallback computes the c5 loss and gradient at full size.
 """
 import hashlib
 import os
@@ -27,26 +32,28 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from graf_inputs import CONFIGS, config_waveforms  # noqa: E402
+from graf_inputs import CONFIGS, config_waveforms, lfm  # noqa: E402
 from oracle import graf_oracle as O  # noqa: E402
 
 
 def main():
     cfg = CONFIGS[5]
     N, M = cfg["N"], cfg["M"]
-    s = config_waveforms(5, batch=1)[0]
+    use_lfm = "--lfm" in sys.argv
+    s = lfm(N, 1.0) if use_lfm else config_waveforms(5, batch=1)[0]
     spec = O.LossSpec.from_dict(dict(cfg["loss"], lambda_isl=0.0, lambda_psl=1.0))
     t0 = time.time()
     L, g, t = O.loss_and_grad_chunked(s, M, spec, chunk_rows=512, chunk_bins=M)
     el = time.time() - t0
-    out = os.path.join(ROOT, "tests", "golden", "c5_w0_softpsl.npz")
+    out = os.path.join(ROOT, "tests", "golden", "c5_lfm_softpsl.npz" if use_lfm else "c5_w0_softpsl.npz")
     np.savez_compressed(
         out, s_sha256=np.array(hashlib.sha256(np.ascontiguousarray(s).tobytes()).hexdigest()),
         N=N, M=M, temperature=spec.temperature, lse=t["lse"], isl=t["isl"], S=t["S"], c=t["c"], Z=t["Z"],
         E=t["E"], count=t["count"], sigma_g=t["sigma_g"], loss_softpsl=L, loss_c5=t["isl"] + t["lse"],
         grad=g.astype(np.complex128), seconds=el,
-        note=np.array("oracle/graf_oracle.py loss_and_grad_chunked, waveform 0 of config 5, "
-                      "lambda_isl=0 lambda_psl=1 T=0.01 full plane minus origin, normalised"))
+        note=np.array("oracle/graf_oracle.py loss_and_grad_chunked, "
+                      + ("LFM chirp lfm(16384, 1.0)" if use_lfm else "waveform 0 of config 5")
+                      + ", lambda_isl=0 lambda_psl=1 T=0.01 full plane minus origin, normalised"))
     print(f"wrote {out} in {el:.0f} s: lse={t['lse']!r} isl={t['isl']!r} max|g|={np.abs(g).max():.3e}")
 
 

@@ -199,6 +199,30 @@ def test_c5_full_size_against_golden(lam_isl):
     gate(f"c5 full size golden lam_isl={lam_isl}", lo.item(), L_ref, g.cpu().numpy()[0], z["grad"])
 
 
+GOLDEN_LFM = os.path.join(os.path.dirname(__file__), "golden", "c5_lfm_softpsl.npz")
+
+
+@pytest.mark.parametrize("lam_isl", [0.0, 1.0])
+def test_c5_full_size_lfm_fallback_against_golden(lam_isl):
+    """c5's spec on an LFM chirp at N = M = 16384 (tests/golden/c5_lfm_softpsl.npz, written by
+    scripts/make_c5_golden.py --lfm from oracle/ only).  Its ridge breaks the R13 rule
+    (max x - xbar >> 40 T), so the optimistic single pass is discarded on the device and the
+    guarded two-pass fallback produces the loss and gradient: the general epilogue (MUFU
+    exp, no polynomial fast form) at full size."""
+    if not os.path.exists(GOLDEN_LFM):
+        pytest.skip("tests/golden/c5_lfm_softpsl.npz missing (scripts/make_c5_golden.py --lfm)")
+    from graf_inputs import lfm
+    z = np.load(GOLDEN_LFM)
+    M = int(z["M"])
+    s = lfm(M, 1.0)[None, :]
+    import hashlib
+    assert str(z["s_sha256"]) == hashlib.sha256(np.ascontiguousarray(s[0]).tobytes()).hexdigest()
+    spec_d = dict(CONFIGS[5]["loss"], lambda_isl=lam_isl)
+    lo, g, _ = graf.af_loss_grad(dev(s), M, graf.LossSpec.from_dict(spec_d))
+    L_ref = float(z["loss_c5"]) if lam_isl else float(z["loss_softpsl"])
+    gate(f"c5 full size LFM (fallback) lam_isl={lam_isl}", lo.item(), L_ref, g.cpu().numpy()[0], z["grad"])
+
+
 @pytest.mark.parametrize("G", [2, 4])
 def test_c5_full_size_sharded_against_golden(G):
     s, z = _golden()
