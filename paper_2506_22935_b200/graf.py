@@ -308,8 +308,15 @@ def af(s, M, layout="centered", k_begin=None, k_end=None, periodic=False):
     return AF.apply(s, M, layout, k_begin, k_end, periodic)
 
 
-def af_loss(s, M, spec: LossSpec, periodic=False):
-    return AFLoss.apply(s, M, spec, periodic)
+def af_loss(s, M, spec: LossSpec, periodic=False, *, shard=None, group=None, backend=None):
+    """Differentiable per-waveform loss.  shard = None: one device; "delay" / "batch": the
+    torch.distributed layers of sharding.py (ShardedAFLoss), aperiodic."""
+    if shard is None:
+        return AFLoss.apply(s, M, spec, periodic)
+    if periodic:
+        raise ValueError("the sharded losses run the aperiodic surface")
+    from .sharding import sharded_af_loss
+    return sharded_af_loss(s, M, spec, shard=shard, group=group, backend=backend)
 
 
 # ---------------------------------------------------------------------------

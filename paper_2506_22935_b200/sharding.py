@@ -39,7 +39,8 @@ import torch.distributed as dist
 
 from . import graf as _graf
 
-__all__ = ["GrafBackend", "batch_slice", "batch_sharded_loss_grad", "delay_sharded_loss_grad"]
+__all__ = ["GrafBackend", "batch_slice", "batch_sharded_loss_grad", "delay_sharded_loss_grad", "ShardedAFLoss",
+           "sharded_af_loss"]
 
 
 class GrafBackend:
@@ -153,3 +154,44 @@ def delay_sharded_loss_grad(s: torch.Tensor, M: int, spec, group=None, backend=N
     loss, g = backend.loss_grad(s, M, spec, glob, shard)
     dist.all_reduce(torch.view_as_real(g), op=dist.ReduceOp.SUM, group=group)
     return loss, g
+
+
+class ShardedAFLoss(torch.autograd.Function):
+    """Differentiable sharded loss (SURVEY.md §8(b) "Python (L3)": af_loss(s, M, spec, group,
+    shard)).  Every rank passes the whole batch s [B, N].
+      shard="delay": the loss of every waveform, identical on all ranks, and in backward the
+        full gradient (the forward's all_reduce already summed the shards) on every rank.
+      shard="batch": this rank's block of waveforms only (no collective); the
+        loss of that block, and in backward a gradient that is zero outside the block (sum
+        s.grad over the ranks, as data-parallel training does, for the whole batch's).
+    torch's convention: .grad = 2 dL/ds* (the ABI returns dL/ds*)."""
+
+    @staticmethod
+    def forward(ctx, s, M, spec, shard, group, backend):
+        if shard == "delay":
+            loss, g = delay_sharded_loss_grad(s.detach(), M, spec, group=group, backend=backend)
+            ctx.block = None
+        elif shard == "batch":
+            sl, loss, g = batch_sharded_loss_grad(s.detach(), M, spec, group=group, backend=backend)
+            ctx.block = (sl.start, sl.stop)
+        else:
+            raise ValueError(f"shard must be 'delay' or 'batch', not {shard!r}")
+        ctx.save_for_backward(g)
+        ctx.s_meta = (s.shape, s.dtype)
+        return loss
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (g,) = ctx.saved_tensors
+        shape, dtype = ctx.s_meta
+        gl = (2.0 * grad_out.to(g.real.dtype)[:, None] * g).to(dtype)
+        if ctx.block is None:
+            return gl, None, None, None, None, None
+        gs = torch.zeros(shape, dtype=dtype, device=g.device)
+        gs[ctx.block[0]:ctx.block[1]] = gl
+        return gs, None, None, None, None, None
+
+
+def sharded_af_loss(s, M, spec, shard="delay", group=None, backend=None):
+    """ShardedAFLoss.apply with keyword defaults (see the class)."""
+    return ShardedAFLoss.apply(s, M, spec, shard, group, backend)

@@ -332,3 +332,55 @@ def test_batch_slice_partition():
             assert sl[0].start == 0 and sl[-1].stop == B
             assert all(sl[i].stop == sl[i + 1].start for i in range(G - 1))
             assert max(x.stop - x.start for x in sl) - min(x.stop - x.start for x in sl) <= 1
+
+
+def _autograd_worker(rank, world, port, shard, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_22935_b200 import LossSpec, graf
+        N, M = 12, 16
+        spec_d = dict(k_max=11, d_max=8, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05,
+                      normalize=1)
+        s = torch.tensor(np.stack([complex_gaussian(SplitMix64(950 + b), N) for b in range(3)]).astype(np.complex128),
+                         requires_grad=True)
+        loss = graf.af_loss(s, M, LossSpec.from_dict(spec_d), shard=shard, backend=OracleShardBackend(N, M))
+        (loss * torch.arange(1, loss.shape[0] + 1, dtype=loss.dtype)).sum().backward()
+        q.put((rank, loss.detach().numpy(), s.grad.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shard", ["delay", "batch"])
+def test_sharded_af_loss_autograd_gloo_world2(shard):
+    """graf.af_loss(..., shard=) (sharding.ShardedAFLoss) on world_size 2 with the oracle
+    backend: the loss and torch's .grad = 2 dL/ds* against the unsharded float64 oracle,
+    with a non-uniform upstream gradient (weights 1, 2, ... per waveform)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_autograd_worker, args=(r, 2, port, shard, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N, M = 12, 16
+    spec_d = dict(k_max=11, d_max=8, ml_k=0, ml_d=1, lambda_isl=1.0, lambda_psl=1.0, temperature=0.05, normalize=1)
+    s = np.stack([complex_gaussian(SplitMix64(950 + b), N) for b in range(3)]).astype(np.complex128)
+    refs = [O.loss_and_grad(s[b], M, O.LossSpec.from_dict(spec_d)) for b in range(3)]
+    L_ref = np.array([r[0] for r in refs])
+    g_ref = np.stack([r[1] for r in refs])
+    from paper_2506_22935_b200.sharding import batch_slice
+    total = np.zeros_like(g_ref)
+    for rank, loss, grad in res:
+        sl = slice(None) if shard == "delay" else batch_slice(3, rank, 2)
+        np.testing.assert_allclose(loss, L_ref[sl], rtol=1e-10)
+        w = np.arange(1, len(loss) + 1)          # the worker's upstream weights on ITS loss vector
+        want = np.zeros_like(g_ref)
+        want[sl] = 2.0 * w[:, None] * g_ref[sl]
+        np.testing.assert_allclose(grad, want, atol=1e-10 * np.abs(want).max())
+        total += grad
+    if shard == "batch":   # the ranks' gradients are disjoint blocks that tile the batch
+        assert np.all(total != 0)
