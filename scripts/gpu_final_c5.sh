@@ -21,4 +21,4 @@ ncu -i gpurun_out/prof_${TAG}_c5.ncu-rep --page source --csv --print-source sass
 python scripts/ncu_phases.py gpurun_out/sass_${TAG}_c5.csv > gpurun_out/phases_${TAG}_c5.txt 2>&1
 rm -f gpurun_out/sass_${TAG}_c5.csv
 SZ=$(stat -c %s gpurun_out/prof_${TAG}_c5.ncu-rep 2>/dev/null || echo 0)
-if [ "$SZ" -gt 25000000 ]; then rm -f gpurun_out/prof_${TAG}_c5.ncu-rep; fi
+if [ -z "$KEEP_REP" ] && [ "$SZ" -gt 25000000 ]; then rm -f gpurun_out/prof_${TAG}_c5.ncu-rep; fi
