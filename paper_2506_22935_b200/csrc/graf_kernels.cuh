@@ -581,6 +581,9 @@ __device__ __forceinline__ void tmem_wait_ldc<8>(float (&r)[8]) { tmem_wait_ld8(
 #ifndef GRAF_SOWN_TMEM_16384
 #define GRAF_SOWN_TMEM_16384 1   // M = 16384 gradient kernels: own samples in TMEM (see kSown)
 #endif
+#ifndef GRAF_LAZY_MASKS
+#define GRAF_LAZY_MASKS 1
+#endif
 #ifndef GRAF_TMEM_SLOTS
 #define GRAF_TMEM_SLOTS 8    // slots per TMEM read-modify-write chunk in the correlation (8 or 4)
 #endif
@@ -802,15 +805,26 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
   using Mask = typename std::conditional<(E > 32), unsigned long long, unsigned>::type;
   using VMask = Mask;
+  // (M >= 8192, GRAF_LAZY_MASKS: not kept in registers across the FFTs; each use tests the
+  // slot's |d| against the limit from the per-row copy of the thread index instead)
+  constexpr bool kLazyMask = (M >= 8192) && GRAF_LAZY_MASKS;
   Mask band = 0, mlb = 0;
+  if constexpr (!kLazyMask) {
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int m = t0 + e * T;
-    const int d = m < M / 2 ? m : m - M;
-    const int ad = d < 0 ? -d : d;
-    band |= (Mask)(ad <= p.d_max ? 1 : 0) << e;
-    mlb |= (Mask)(ad <= p.ml_d ? 1 : 0) << e;
+    for (int e = 0; e < E; ++e) {
+      const int m = t0 + e * T;
+      const int d = m < M / 2 ? m : m - M;
+      const int ad = d < 0 ? -d : d;
+      band |= (Mask)(ad <= p.d_max ? 1 : 0) << e;
+      mlb |= (Mask)(ad <= p.ml_d ? 1 : 0) << e;
+    }
   }
+  // |d| of slot e of thread tt (centred Doppler distance of frequency m = tt + e T)
+  auto adop = [&](int tt, int e) {
+    const int m = tt + e * T;
+    const int d = m < M / 2 ? m : m - M;
+    return d < 0 ? -d : d;
+  };
   // split write-after-read barrier of the exchange buffer (one-slot CTAs; not when the
   // surface staging is aliased onto the exchange buffer, p.bulk == 2)
   const uint32_t war_mb = smem_u32(red + 62);
@@ -969,7 +983,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           }
           const int m = t + e * T;
           const int d = m < M / 2 ? m : m - M;
-          v[e] = (valid && ((band >> e) & 1)) ? crow[d] : make_float2(0.f, 0.f);
+          v[e] = (valid && (kLazyMask ? adop(t, e) <= p.d_max : ((band >> e) & 1))) ? crow[d] : make_float2(0.f, 0.f);
         }
       } else {
       if constexpr (!SPLIT) {
@@ -1078,7 +1092,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
           if (eb && e != 0 && e != E - 1) continue;
           const int m = t + e * T;
           const int d = m < M / 2 ? m : m - M;
-          if ((band >> e) & 1) crow[d] = v[e];
+          if (kLazyMask ? adop(t, e) <= p.d_max : ((band >> e) & 1)) crow[d] = v[e];
         }
       }
       }
@@ -1182,6 +1196,15 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       //      out-of-region value may overflow).
       if (lrow) {
         const Mask inm = band & ~((k < 0 ? -k : k) <= p.ml_k ? mlb : (Mask)0);   // (CROSS rows may be k < 0)
+        const bool kml = (k < 0 ? -k : k) <= p.ml_k;                            // (kLazyMask)
+        auto in_region = [&](int e) -> bool {
+          if constexpr (kLazyMask) {
+            const int ad = adop(t, e);
+            return ad <= p.d_max && !(kml && ad <= p.ml_d);
+          } else {
+            return (inm >> e) & 1;
+          }
+        };
         const float wk = WGT && p.w_k ? p.w_k[k + N - 1] : 1.f;
         float rowS = 0.f, rowM = -INFINITY, rowF = 0.f, rowMt = 0.f, rowC1 = 0.f, rowM1 = -INFINITY, rowX = 0.f;
         const float gsc = scaleG * mult;
@@ -1198,7 +1221,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
             for (int e = 0; e < E; ++e) {
               const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
-              rowX += ((mlb >> e) & 1) ? chi : 0.f;
+              rowX += (kLazyMask ? adop(t, e) <= p.ml_d : ((mlb >> e) & 1)) ? chi : 0.f;
             }
           }
         }
@@ -1265,7 +1288,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           if (eb && e != 0 && e != E - 1) continue;   // outside the band: no term, G unused
-          const bool in = (inm >> e) & 1;
+          const bool in = in_region(e);
           float w = 1.f;
           if constexpr (WGT) {
             const int m = t + e * T;
@@ -1345,7 +1368,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
 #pragma unroll
             for (int e = 0; e < E; ++e) {
               if (eb && e != 0 && e != E - 1) continue;
-              const bool in = (inm >> e) & 1;
+              const bool in = in_region(e);
               const float chi = v[e].x * v[e].x + v[e].y * v[e].y;
               const float x = p.normalize ? chi * invE2 : chi;
               const float z = exp_fast((x - accM) * p.invT);
