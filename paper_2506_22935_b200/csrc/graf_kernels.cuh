@@ -584,6 +584,9 @@ __device__ __forceinline__ void tmem_wait_ldc<8>(float (&r)[8]) { tmem_wait_ld8(
 #ifndef GRAF_LAZY_MASKS
 #define GRAF_LAZY_MASKS 1
 #endif
+#ifndef GRAF_ACC_TMEM_8192
+#define GRAF_ACC_TMEM_8192 1
+#endif
 #ifndef GRAF_TMEM_SLOTS
 #define GRAF_TMEM_SLOTS 8    // slots per TMEM read-modify-write chunk in the correlation (8 or 4)
 #endif
@@ -794,12 +797,19 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   constexpr bool kTwTmem = kTmem && !kSown && (M == 16384) && !SPLIT && GRAF_TW1_TMEM_16384 && (E == 32) &&
                            (num_passes(M, E) >= 2) && (pass_radix(M, E, 1) == 32);
   constexpr int kTmemNC = 2 * E * (THREADS / 128) * ((kTwTmem || kSown) ? 2 : 1);
+  // (M = 8192, GRAF_ACC_TMEM_8192: the per-thread running sums of the loss partials live in 16
+  // tensor-memory columns per thread instead of registers, loaded at each loss row's epilogue and
+  // stored back, so they are not live, and not spilled to local memory, across the FFTs: with
+  // two 105 KiB CTAs per SM the small L1 sends spill reloads to L2)
+  constexpr bool kAccTm = (M == 8192) && !CROSS && (KIND != K_ADJ) && (S == 1) && GRAF_ACC_TMEM_8192;
+  constexpr int kAccCol = kTmem ? kTmemNC : 0;                    // the running sums' column block
+  constexpr int kAllocNC = kTmem ? (kAccTm ? 2 * kTmemNC : kTmemNC) : (kAccTm ? 16 * (THREADS / 128) : 0);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 60);
-  if constexpr (kTmem) {
+  if constexpr (kTmem || kAccTm) {
     static_assert(THREADS % 128 == 0 && (E % 8) == 0, "TMEM accumulator layout: whole lane quarters");
-    static_assert(kTmemNC == 32 || kTmemNC == 64 || kTmemNC == 128 || kTmemNC == 256 || kTmemNC == 512,
+    static_assert(kAllocNC == 32 || kAllocNC == 64 || kAllocNC == 128 || kAllocNC == 256 || kAllocNC == 512,
                   "TMEM allocation: a power of two >= 32 columns");
-    if (warp == 0) tmem_alloc<kTmemNC>(tslot);
+    if (warp == 0) tmem_alloc<kAllocNC>(tslot);
     tmem_fence_before();
   }
   // per-thread Doppler masks (depend on the slot's frequency m = t + e*T only)
@@ -875,6 +885,11 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     }
     tmem_wait_st();
   }
+  uint32_t tacs = 0;   // kAccTm: this thread's 16 running-sum columns
+  if constexpr (kAccTm) {
+    if constexpr (!kTmem) tmem_fence_after();
+    tacs = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(kAccCol + 16 * (warp >> 2));
+  }
   const double Ed = red[0];
   // CROSS: normalisation by E1 E2 (reading R25); invE = 1/sqrt(E1 E2) for the surface
   const double Ed2 = CROSS ? red[1] : Ed;
@@ -923,6 +938,40 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   float accM = -INFINITY;
   float argX = -INFINITY;   // hard-PSL argmax (value, key) of this thread
   int argK = 0x7fffffff;
+  // kAccTm: [S, F, Z, C, Mt as (lo, hi) pairs, M, argX, argK] in the thread's 16 TMEM columns
+  auto acc_store = [&]() {
+    if constexpr (kAccTm) {
+      float r[16];
+      const double dv[5] = {accS, accF, accZ, accC, accMt};
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        r[2 * i] = __int_as_float(__double2loint(dv[i]));
+        r[2 * i + 1] = __int_as_float(__double2hiint(dv[i]));
+      }
+      r[10] = accM;
+      r[11] = argX;
+      r[12] = __int_as_float(argK);
+      r[13] = r[14] = r[15] = 0.f;
+      tmem_st16(tacs, r);
+    }
+  };
+  auto acc_load = [&]() {
+    if constexpr (kAccTm) {
+      tmem_wait_st();
+      float r[16];
+      tmem_ld16(tacs, r);
+      tmem_wait_ld16(r);
+      accS = __hiloint2double(__float_as_int(r[1]), __float_as_int(r[0]));
+      accF = __hiloint2double(__float_as_int(r[3]), __float_as_int(r[2]));
+      accZ = __hiloint2double(__float_as_int(r[5]), __float_as_int(r[4]));
+      accC = __hiloint2double(__float_as_int(r[7]), __float_as_int(r[6]));
+      accMt = __hiloint2double(__float_as_int(r[9]), __float_as_int(r[8]));
+      accM = r[10];
+      argX = r[11];
+      argK = __float_as_int(r[12]);
+    }
+  };
+  acc_store();
 
   const int rows_per_iter = P * S;
   const int iters = (p.U + rows_per_iter - 1) / rows_per_iter;
@@ -1195,6 +1244,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
       //      slots: out-of-region slots select 0 (never multiply: exp of an
       //      out-of-region value may overflow).
       if (lrow) {
+        acc_load();
         const Mask inm = band & ~((k < 0 ? -k : k) <= p.ml_k ? mlb : (Mask)0);   // (CROSS rows may be k < 0)
         const bool kml = (k < 0 ? -k : k) <= p.ml_k;                            // (kLazyMask)
         auto in_region = [&](int e) -> bool {
@@ -1384,6 +1434,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
             accM = fmaxf(accM, rowM);
           }
         }
+        acc_store();
       } else if constexpr (GRAD) {
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
@@ -1693,6 +1744,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   double* scratch = reinterpret_cast<double*>(xch);  // exchange space is free now
   double* rec = p.fuse ? red + 8 : p.part + ((size_t)b * P + pb) * kPart;
   if constexpr (KIND != K_ADJ) {
+    acc_load();
     const double S0 = block_sum<THREADS>(accS, scratch);
     const double F0 = block_sum<THREADS>(accF, scratch);
     double Z0 = 0.0, C0 = 0.0;
@@ -1769,7 +1821,14 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
     __syncthreads();
     if (warp == 0) {
       tmem_fence_after();
-      tmem_dealloc<kTmemNC>(*tslot);
+      tmem_dealloc<kAllocNC>(*tslot);
+    }
+  } else if constexpr (kAccTm) {
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc<kAllocNC>(*tslot);
     }
   }
 
