@@ -668,7 +668,7 @@ __device__ __forceinline__ unsigned long long slot_range_mask(int e_lo, int e_hi
 // with s) accumulated separately.
 // FLV (flavour, M >= 8192 where the register budget is tight; the host picks it per call):
 //   0 the general kernel;  1 loss-only, the surface epilogue compiled out (c4 -6 %, c5 -2.5 %,
-//   profiles/r02/tune_nosurf.txt).  (A third flavour with only the full-plane single pass
+//   profiles/r02/tune_nosurf.txt);  2 loss-only on a band narrower than T bins (c4).  (A third flavour with only the full-plane single pass
 //   compiled in spilled 352 B and measured 14.68 ms against 12.65: not kept.)
 template <int M, int KIND, bool WGT, bool CROSS = false, int FLV = 0>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af_rows_kernel(RowParams p) {
@@ -721,10 +721,13 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, MinBlocks<M, KIND>::value) af
   // only (M >= 2048, first pass one radix-E butterfly)
   constexpr bool kEdgeBand = kHalfSizes && (KIND == K_ISL || KIND == K_PASS2 || KIND == K_MATCH) &&
                              pass_radix(M, E, 0) == E && E <= GRAF_MAX_RADIX && num_passes(M, E) > 1;
-  const bool edge_band = kEdgeBand && p.d_max < T;
+  // (FLV 2: the loss band is known to be narrower than T bins, |d| <= d_max < T; the host
+  // launches it only then, so the band-edge forms are compile-time and the other slots'
+  // epilogue code is not compiled)
+  const bool edge_band = kEdgeBand && (FLV == 2 || p.d_max < T);
   // ... and the loss epilogues, the band cache and (pass 1) the loss statistics then touch
   // slots 0 and E - 1 only (the others are outside the band: their terms are 0)
-  const bool eb = FWD ? (kHalfSizes && p.d_max < T) : edge_band;
+  const bool eb = FWD ? (kHalfSizes && (FLV == 2 || p.d_max < T)) : edge_band;
   constexpr bool kEdgeFwd = kHalfSizes && FWD && num_passes(M, E) >= 3 && !Twiddles<C::MX, E2>::CACHE;
   // s[n] at sv_o + n with sv_o + n 16-byte aligned for ODD n (the shifted copy)
   const float2* sv_o = C::S_SMEM ? sv : p.s_pad1 + (size_t)b * RP + NL + 1;

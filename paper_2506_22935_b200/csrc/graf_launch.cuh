@@ -207,10 +207,24 @@ cudaError_t launch_rows_t(Plan& pl, const RowParams& rp, int B, cudaStream_t st,
 #ifndef GRAF_NOSURF_SPEC
 #define GRAF_NOSURF_SPEC 1
 #endif
+#ifndef GRAF_EDGE_FLAVOUR
+#define GRAF_EDGE_FLAVOUR 1
+#endif
 #ifndef GRAF_NOSURF_MIN_M
 #define GRAF_NOSURF_MIN_M 8192
 #endif
   if constexpr (M >= GRAF_NOSURF_MIN_M && GRAF_NOSURF_SPEC) {
+    if (rp.surface == nullptr && GRAF_EDGE_FLAVOUR && rp.loss_on && rp.d_max < Cfg<M>::T && !wgt) {
+      // loss-only on a band narrower than T bins (c4): the band-edge flavour
+      switch (kind) {
+        case K_FWD:
+          if (!rp.want_argmax) return launch_kernel<M, K_FWD, false, false, 2>(pl, rp, B, st);
+          break;
+        case K_PASS2: return launch_kernel<M, K_PASS2, false, false, 2>(pl, rp, B, st);
+        case K_ISL: return launch_kernel<M, K_ISL, false, false, 2>(pl, rp, B, st);
+        default: break;
+      }
+    }
     if (rp.surface == nullptr) {   // loss-only calls: the instantiations without the surface epilogue
       switch (kind) {
         case K_FWD:
