@@ -887,7 +887,7 @@ static graf_status impl_sp_begin(const graf_af_desc* af, const graf_loss_desc* L
     fc.gpart = f.gpart + b0 * f.P * (long long)af->n;
     fc.rec1 = f.rec1 + b0 * kPart;
     fc.gsum = f.gsum + b0 * af->n;
-    sp_fold_kernel<<<(unsigned)nb, 256, 0, cs>>>(fc);
+    sp_fold_kernel<<<dim3((unsigned)nb, (unsigned)((af->n + 255) / 256)), 256, 0, cs>>>(fc);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "sp_fold_kernel launch");
     ++t_launches;
   }

@@ -2124,9 +2124,12 @@ struct SpFoldParams {
   float T;
 };
 
+// grid (B, ceil(N / 256)): one CTA per waveform and 256-sample chunk, so the fold of c5's
+// 8 x 37 x 16384 partial-gradient entries runs on every SM (round 2's first version ran one
+// CTA per waveform: 0.40 ms of a 2.05 ms G = 8 shard step; profiles/r02/shard_times.txt)
 __global__ void __launch_bounds__(256) sp_fold_kernel(SpFoldParams f) {
   const int b = blockIdx.x;
-  if (threadIdx.x == 0) {
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
     double S = 0, Z = 0, C = 0, F = 0, Mt = 0, m = -INFINITY;
     for (int q = 0; q < f.P; ++q) {
       const double* rec = f.part + ((size_t)b * f.P + q) * kPart;
@@ -2146,15 +2149,27 @@ __global__ void __launch_bounds__(256) sp_fold_kernel(SpFoldParams f) {
     o[6] = Mt;
     o[7] = 0.0;
   }
-  for (int n = threadIdx.x; n < f.N; n += blockDim.x) {
-    double gx = 0, gy = 0;
-    for (int q = 0; q < f.P; ++q) {
-      const float2 a = f.gpart[((size_t)b * f.P + q) * f.N + n];
-      gx += a.x;
-      gy += a.y;
+  const int n = blockIdx.y * blockDim.x + threadIdx.x;
+  if (n >= f.N) return;
+  const float2* gp = f.gpart + (size_t)b * f.P * f.N + n;
+  double gx = 0, gy = 0;
+  int q = 0;
+  for (; q + 8 <= f.P; q += 8) {   // 8 loads in flight, summed in the fixed order q = 0, 1, ...
+    float2 a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = gp[(size_t)(q + i) * f.N];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      gx += a[i].x;
+      gy += a[i].y;
     }
-    f.gsum[(size_t)b * f.N + n] = make_float2((float)gx, (float)gy);
   }
+  for (; q < f.P; ++q) {
+    const float2 a = gp[(size_t)q * f.N];
+    gx += a.x;
+    gy += a.y;
+  }
+  f.gsum[(size_t)b * f.N + n] = make_float2((float)gx, (float)gy);
 }
 
 // Phase 2 head: the R13 validity rule on the GLOBAL (rank-order combined) partials.
