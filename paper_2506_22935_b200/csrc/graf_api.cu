@@ -321,7 +321,10 @@ Plan make_plan(const graf_af_desc* af, const graf_loss_desc* L, Kind kind, bool 
   // actual P <= bound from the kernel's measured occupancy (choose_P).
   const long long B = af->batch;
   const long long maxP = std::max(1, (pl.U + ci.S - 1) / ci.S);
-  const long long capP = std::max(1LL, (long long)(device_sm_count() * 8 + B - 1) / B);
+#ifndef GRAF_CAP_MULT
+#define GRAF_CAP_MULT 8   // CTAs per SM (summed over the batch) that bound P; tuning builds override it
+#endif
+  const long long capP = std::max(1LL, (long long)(device_sm_count() * GRAF_CAP_MULT + B - 1) / B);
   pl.P = (int)std::max(1LL, std::min(maxP, capP));
   pl.Pbound = pl.P;
   size_t off = 0;

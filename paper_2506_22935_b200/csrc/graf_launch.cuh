@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -64,21 +65,46 @@ struct Plan {
 
 
 // Cost model: waves x (row iterations + CTA setup), setup ~ one row iteration.
+// Candidates within 2 % of the best are then ranked by a second model in which the last,
+// partial wave is cheaper than a full one: its CTAs share their SM with fewer neighbours
+// (j of occ resident), and a throughput-bound CTA then runs in about (j / occ)^0.75 of the
+// time.  Measured on c3's half batch (B = 512, scripts/p_variants.sh): the plain model
+// ties P = 1 (514) with P = 2 (516) and took P = 1 at 3.13 ms; P = 2 runs in 2.89 ms.  The
+// discount is only a tie-break because latency-bound kernels (c2) do not speed up alone.
 inline int choose_P(const Plan& pl, long long B, int occ, int nsm) {
-  const long long cap = (long long)nsm * std::max(occ, 1);
+  const int oc = std::max(occ, 1);
+  const long long cap = (long long)nsm * oc;
   int best = 1;
   double best_t = 1e300;
-  for (int P = 1; P <= pl.Pbound; ++P) {
+  auto plain = [&](int P) {
     const long long ctas = (long long)P * B;
     const double waves = (double)((ctas + cap - 1) / cap);
     const double iters = (double)((pl.U + (long long)P * pl.S - 1) / ((long long)P * pl.S));
-    const double t = waves * (iters + 1.0);
+    return waves * (iters + 1.0);
+  };
+  for (int P = 1; P <= pl.Pbound; ++P) {
+    const double t = plain(P);
     if (t < best_t - 1e-9) {
       best_t = t;
       best = P;
     }
   }
-  return best;
+  int pick = best;
+  double pick_t = 1e300;
+  for (int P = 1; P <= pl.Pbound; ++P) {
+    if (plain(P) > 1.02 * best_t) continue;
+    const long long ctas = (long long)P * B;
+    const long long full = ctas / cap, rest = ctas - full * cap;
+    const double j = (double)((rest + nsm - 1) / nsm);   // CTAs per SM in the partial wave
+    const double waves = (double)full + (rest ? pow(j / (double)oc, 0.75) : 0.0);
+    const double iters = (double)((pl.U + (long long)P * pl.S - 1) / ((long long)P * pl.S));
+    const double t = waves * (iters + 1.0);
+    if (t < pick_t - 1e-9) {
+      pick_t = t;
+      pick = P;
+    }
+  }
+  return pick;
 }
 
 template <int M, int KIND, bool WGT, bool CROSS = false, int FLV = 0>
