@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -123,8 +124,17 @@ cudaError_t kernel_occupancy(size_t smem, int* occ, int* nsm) {
   });
   if (attr_err[dev] != cudaSuccess) return attr_err[dev];
   *nsm = sm_count[dev];
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT, CROSS, FLV>, Cfg<M>::THREADS,
-                                                       smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, af_rows_kernel<M, KIND, WGT, CROSS, FLV>, Cfg<M>::THREADS, smem);
+  if (e != cudaSuccess) return e;
+  // The occupancy API reported 1 for the M = 8192 kernels (2 x 104 832 B of dynamic shared
+  // memory) although two CTAs are resident per SM (ncu: launch__occupancy_limit_shared_mem and
+  // _registers = 2; scripts/block_one.py), so the launch model planned c4's blocks for 148
+  // slots instead of 296.  __launch_bounds__ guarantees registers and threads for MinBlocks
+  // CTAs; with the SM's 228 KiB of shared memory (1 KiB reserved per CTA) that is a lower
+  // bound on the resident CTAs.
+  const int by_smem = (int)((228 * 1024) / (smem + 1024));
+  *occ = std::max(*occ, std::min(MinBlocks<M, KIND>::value, by_smem));
+  return cudaSuccess;
 }
 
 template <int M, int KIND, bool WGT, bool CROSS = false, int FLV = 0>
@@ -178,6 +188,10 @@ cudaError_t launch_kernel(Plan& pl, RowParams rp, int B, cudaStream_t st) {
     pl.P = std::min(GRAF_FORCE_P, std::max(pl.Pbound, 1));
 #endif
     pl.fixedP = true;   // later passes of the same call reuse it
+#ifdef GRAF_DEBUG_PLAN   // tuning builds only: what the launch model saw and chose
+    fprintf(stderr, "[graf plan] M=%d kind=%d flv=%d B=%d U=%d S=%d occ=%d nsm=%d Pbound=%d P=%d smem=%zu\n", M, KIND, FLV, B,
+            pl.U, pl.S, occ, nsm, pl.Pbound, pl.P, smem);
+#endif
   }
   rp.fuse = 0;
   if (KIND == K_ISL && !CROSS && Cfg<M>::G_SMEM && pl.fuse_req && pl.P >= 2 && pl.P <= 8) {   // (P = 1: measured slower as a cluster launch)
