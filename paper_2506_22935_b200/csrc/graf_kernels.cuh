@@ -2126,7 +2126,7 @@ struct SpFoldParams {
 
 // grid (B, ceil(N / 256)): one CTA per waveform and 256-sample chunk, so the fold of c5's
 // 8 x 37 x 16384 partial-gradient entries runs on every SM (round 2's first version ran one
-// CTA per waveform: 0.40 ms of a 2.05 ms G = 8 shard step; profiles/r02/shard_times.txt)
+// CTA per waveform: 0.40 ms of a 2.05 ms G = 8 shard step; profiles/r02/shard/)
 __global__ void __launch_bounds__(256) sp_fold_kernel(SpFoldParams f) {
   const int b = blockIdx.x;
   if (blockIdx.y == 0 && threadIdx.x == 0) {
