@@ -284,6 +284,14 @@ graf_status graf_combine_partials(const graf_loss_desc* loss, const graf_partial
  * ISL call whose finalize runs inside the row kernel; 2 when it runs separately). */
 int32_t graf_last_launch_count(void);
 
+/* Diagnostics (host only, no CUDA call): the CTAs per waveform P that the launch model
+ * (choose_P, csrc/graf_launch.cuh) picks for `rows` delay rows per
+ * waveform, `slots` row slots per CTA, a batch of `batch` waveforms, `occ` resident CTAs
+ * per SM on `nsm` SMs, from the candidates 1..p_bound.  Returns 0 for a non-positive
+ * argument.  The production launches call the same function with the kernel's occupancy. */
+int32_t graf_plan_ctas_per_waveform(int32_t rows, int32_t slots, int64_t batch, int32_t occ,
+                                    int32_t nsm, int32_t p_bound);
+
 /* Diagnostics: with both events non-NULL (cudaEvent_t handles created by the
  * caller), every later entry-point call made by THIS thread records `start` on
  * its stream just before its first delay-row kernel (af_rows_kernel) and `stop`

@@ -20,7 +20,8 @@ EXPORTS = ("graf_abi_version", "graf_status_string", "graf_last_error", "graf_wo
            "graf_set_profile_events", "graf_last_launch_count", "graf_spectral_variance",
            "graf_phase_adam_step", "graf_xaf_workspace_bytes", "graf_xaf_forward", "graf_xaf_loss_grad",
            "graf_xaf_backward", "graf_mainlobe_width", "graf_af_single_pass_eligible",
-           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end", "graf_init", "graf_probe_fp32")
+           "graf_af_loss_grad_sp_begin", "graf_af_loss_grad_sp_end", "graf_init", "graf_probe_fp32",
+           "graf_plan_ctas_per_waveform")
 
 
 class AfDesc(ctypes.Structure):
@@ -111,6 +112,8 @@ def lib() -> ctypes.CDLL:
         L.graf_phase_adam_step.restype = c_int32
         L.graf_phase_adam_step.argtypes = [c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                            c_void_p, c_float, c_float, c_float, c_float, c_void_p]
+        L.graf_plan_ctas_per_waveform.restype = c_int32
+        L.graf_plan_ctas_per_waveform.argtypes = [c_int32, c_int32, c_int64, c_int32, c_int32, c_int32]
         L.graf_last_launch_count.restype = c_int32
         L.graf_last_launch_count.argtypes = []
         L.graf_set_profile_events.restype = c_int32

@@ -645,6 +645,16 @@ const char* graf_last_error(void) { return t_last_error.c_str(); }
 
 int32_t graf_last_launch_count(void) { return t_launches; }
 
+int32_t graf_plan_ctas_per_waveform(int32_t rows, int32_t slots, int64_t batch, int32_t occ, int32_t nsm,
+                                    int32_t p_bound) {
+  if (rows <= 0 || slots <= 0 || batch <= 0 || occ <= 0 || nsm <= 0 || p_bound <= 0) return 0;
+  Plan pl;
+  pl.U = rows;
+  pl.S = slots;
+  pl.Pbound = p_bound;
+  return choose_P(pl, batch, occ, nsm);
+}
+
 static size_t impl_workspace_bytes(const graf_af_desc* af, const graf_loss_desc* loss, bool cross) {
   if (check_af(af) != GRAF_OK) return 0;
   if (loss && check_loss(af, loss) != GRAF_OK) return 0;

@@ -110,3 +110,32 @@ def test_host_combine_partials_is_exact_lse_merge():
     ref = sum(math.exp((x - 0.7) / T) for x in (0.1, 0.3, 0.7))
     assert out.isl_sum == 3.0 and abs(out.lse_max - 0.7) < 1e-7 and abs(out.lse_sum - ref) < 1e-6
     assert out.psl_key == 5.0                      # the argmax cell of the larger max
+
+
+# The launch model (choose_P, csrc/graf_launch.cuh).  Expected values
+# are the CTAs per waveform measured fastest on one B200 (profiles/r01_p_sweep.txt for the
+# full batches, profiles/r02/shard/p_variants_*.txt for the batch-sharded blocks):
+# (rows, slots, batch, resident CTAs per SM, P bound) -> P.
+@pytest.mark.parametrize("rows,slots,batch,occ,p_bound,expect", [
+    (65, 8, 256, 4, 5, 2),          # c2 (fused cluster finalize, P = 2)
+    (1024, 4, 1024, 2, 2, 2),       # c3
+    (1024, 4, 512, 2, 3, 2),        # c3 half batch: the plain wave model ties P = 1 (slower)
+    (513, 1, 64, 2, 19, 9),         # c4
+    (513, 1, 16, 2, 74, 18),        # c4 block of 16: needs occ = 2 (the API reported 1 -> P = 9)
+    (513, 1, 8, 2, 148, 37),        # c4 block of 8
+    (16384, 1, 8, 1, 148, 37),      # c5: 296 CTAs, two waves of one CTA per SM
+    (2048, 1, 8, 1, 148, 37),       # c5, one shard of G = 8
+])
+def test_launch_model_ctas_per_waveform(rows, slots, batch, occ, p_bound, expect):
+    lib = L.lib()
+    assert lib.graf_plan_ctas_per_waveform(rows, slots, batch, occ, 148, p_bound) == expect
+
+
+def test_launch_model_bounds_and_bad_arguments():
+    lib = L.lib()
+    for args in [(0, 1, 1, 1, 148, 1), (1, 0, 1, 1, 148, 1), (1, 1, 0, 1, 148, 1), (1, 1, 1, 0, 148, 1),
+                 (1, 1, 1, 1, 0, 1), (1, 1, 1, 1, 148, 0)]:
+        assert lib.graf_plan_ctas_per_waveform(*args) == 0
+    for rows, slots, batch, occ, pb in [(1, 16, 1, 4, 8), (64, 16, 1, 4, 4), (4095, 2, 3, 2, 400), (513, 1, 64, 2, 1)]:
+        p = lib.graf_plan_ctas_per_waveform(rows, slots, batch, occ, 148, pb)
+        assert 1 <= p <= pb
